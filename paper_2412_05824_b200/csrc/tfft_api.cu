@@ -1,0 +1,644 @@
+// C-ABI layer of libtfft.so (declared in include/tfft.h): plans, dispatch to the
+// K1 single-pass / K3 two-pass kernels, the stage-strike path and the
+// replay-engine primitives.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "../../include/tfft.h"
+#include "tfft_aux.h"
+#include "tfft_internal.h"
+#include "tfft_k3.h"
+
+using namespace tfft;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(int e, const char* what) {
+  if (e == 0) return TFFT_OK;
+  g_err = std::string(what) + ": " + cudaGetErrorString((cudaError_t)e);
+  return e == (int)cudaErrorMemoryAllocation ? TFFT_ENOMEM : TFFT_ECUDA;
+}
+
+#define TFFT_TRY(expr, what)                          \
+  do {                                                \
+    int _e = (expr);                                  \
+    g_launches.fetch_add(1, std::memory_order_relaxed); \
+    if (_e) return cuda_fail(_e, what);               \
+  } while (0)
+
+bool is_pow2(int64_t v) { return v >= 1 && (v & (v - 1)) == 0; }
+int ilog2_64(int64_t v) {
+  int r = 0;
+  while ((int64_t(1) << r) < v) ++r;
+  return r;
+}
+
+// omega_N^k = exp(-2 pi i k / N) in extended precision, rounded once
+void fill_twiddles(std::vector<long double>& re, std::vector<long double>& im, int64_t n) {
+  re.resize(n);
+  im.resize(n);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int64_t k = 0; k < n; ++k) {
+    // reduce to the first octant for accuracy, then use symmetry
+    const long double a = two_pi * (long double)k / (long double)n;
+    re[k] = cosl(a);
+    im[k] = -sinl(a);
+  }
+  // exact values where they are exact
+  for (int64_t k = 0; k < n; k += std::max<int64_t>(n / 4, 1)) {
+    const int64_t q = (k * 4) / n;
+    const long double cs[4] = {1, 0, -1, 0}, sn[4] = {0, -1, 0, 1};
+    if (n % 4 == 0 || k == 0) {
+      re[k] = cs[q];
+      im[k] = sn[q];
+    }
+  }
+  if (n >= 2) {
+    re[n / 2] = -1;
+    im[n / 2] = 0;
+  }
+}
+
+template <typename T>
+void pack(const std::vector<long double>& re, const std::vector<long double>& im, bool conj, std::vector<T>& out) {
+  out.resize(2 * re.size());
+  for (size_t k = 0; k < re.size(); ++k) {
+    out[2 * k] = (T)re[k];
+    out[2 * k + 1] = (T)(conj ? -im[k] : im[k]);
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return (int)e;
+    cap = bytes;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct tfft_plan {
+  int64_t n = 0;
+  int logn = 0;
+  int prec = 0;
+  int64_t bs = 1;
+  std::vector<int64_t> spans;
+  std::vector<int32_t> radices;
+  struct Pass {
+    int64_t s;
+    int r;
+    int stage;
+  };
+  std::vector<Pass> passes;  // the reference's radix-4/2 lowering (fft_core.py:137-202)
+  int num_sms = 148;
+  int device = 0;
+  bool k1 = false;
+  DevBuf tw_fwd, tw_inv;     // omega_N^k, conj (K1 and ABFT encodings)
+  DevBuf rows[3];            // left checksum rows per encoding kind
+  bool row_ready[3] = {false, false, false};
+  DevBuf counters;           // default counters
+  DevBuf faults;
+  DevBuf ws, win_count;
+  DevBuf scratch_a, scratch_b, base;  // strike path
+  DevBuf col_a, col_b, col64;         // single-column work
+  K3Plan* k3 = nullptr;               // two-pass machinery (N beyond K1)
+  tfft_plan* promoted = nullptr;      // FP64 twin for FP32 correction columns
+};
+
+namespace {
+
+size_t cbytes(int prec) { return prec == 0 ? 8 : 16; }
+
+// the reference's radix lowering: micro radix 2^g -> [4]*(g//2) + [2]*(g%2),
+// repeated while the remaining span >= micro, then the remainder
+void lower(tfft_plan* p) {
+  p->passes.clear();
+  int64_t s = 1;
+  for (size_t si = 0; si < p->spans.size(); ++si) {
+    auto micro = [](int64_t radix, std::vector<int>& out) {
+      int g = ilog2_64(radix);
+      for (int i = 0; i < g / 2; ++i) out.push_back(4);
+      if (g % 2) out.push_back(2);
+    };
+    std::vector<int> f;
+    int64_t rest = p->spans[si];
+    while (rest >= p->radices[si]) {
+      micro(p->radices[si], f);
+      rest /= p->radices[si];
+    }
+    if (rest > 1) micro(rest, f);
+    for (int r : f) {
+      p->passes.push_back({s, r, (int)si});
+      s *= r;
+    }
+  }
+}
+
+int upload(DevBuf& b, const void* host, size_t bytes) {
+  int e = b.ensure(bytes);
+  if (e) return e;
+  return (int)cudaMemcpy(b.p, host, bytes, cudaMemcpyHostToDevice);
+}
+
+int ensure_row(tfft_plan* p, int enc) {
+  if (p->row_ready[enc]) return 0;
+  std::vector<unsigned char> host(p->n * cbytes(p->prec));
+  int rc = tfft_left_row(enc, p->n, p->prec, host.data());
+  if (rc) return rc;
+  int e = upload(p->rows[enc], host.data(), host.size());
+  if (e) return cuda_fail(e, "left row upload");
+  p->row_ready[enc] = true;
+  return 0;
+}
+
+// faulted transactions outside K1/K3's in-kernel strike reach: replay them pass
+// by pass through the reference-order kernels (fault.py:99-107 semantics)
+int strike_path(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, int64_t signal_offset,
+                const std::vector<tfft_fault>& fl, cudaStream_t st, std::vector<int64_t>* touched_rows) {
+  const size_t cb = cbytes(p->prec);
+  std::vector<int64_t> done;
+  for (const tfft_fault& f : fl) {
+    const int64_t tx = f.transaction;
+    if (std::find(done.begin(), done.end(), tx) != done.end()) continue;
+    done.push_back(tx);
+    const int64_t a = std::max<int64_t>(tx * p->bs - signal_offset, 0);
+    const int64_t b = std::min<int64_t>((tx + 1) * p->bs - signal_offset, batch);
+    if (a >= b) continue;
+    const int64_t rows = b - a;
+    int e = p->scratch_a.ensure(rows * p->n * cb);
+    if (!e) e = p->scratch_b.ensure(rows * p->n * cb);
+    if (!e) e = p->base.ensure(p->n * cb);
+    if (e) return cuda_fail(e, "strike scratch");
+    TFFT_TRY((int)cudaMemcpyAsync(p->scratch_a.p, (const char*)x + a * p->n * cb, rows * p->n * cb,
+                                  cudaMemcpyDeviceToDevice, st),
+             "strike copy-in");
+    void* cur = p->scratch_a.p;
+    void* nxt = p->scratch_b.p;
+    size_t pi = 0;
+    for (size_t si = 0; si < p->spans.size(); ++si) {
+      for (const tfft_fault& g : fl) {
+        if (g.transaction != tx || g.stage != (int)si) continue;
+        const int64_t r = g.signal - signal_offset - a;
+        if (r < 0 || r >= rows) continue;
+        TFFT_TRY(launch_flip(p->prec, cur, r * p->n + g.element, g.part, g.bit, st), "strike flip");
+      }
+      while (pi < p->passes.size() && p->passes[pi].stage == (int)si) {
+        const auto& ps = p->passes[pi];
+        // base table omega_(s r)^q = omega_N^(q N/(s r)) read with a stride
+        const DevBuf& tw = inverse ? p->tw_inv : p->tw_fwd;
+        const void* base = nullptr;
+        int64_t stride = 0;
+        if (tw.p) {
+          base = tw.p;
+          stride = p->n / (ps.s * ps.r);
+        } else {
+          TFFT_TRY(k3_base_table(p->k3, p->prec, ps.s, ps.r, inverse, p->base.p, st), "strike base table");
+          base = p->base.p;
+          stride = 1;
+        }
+        TFFT_TRY(launch_stockham_pass(p->prec, cur, nxt, rows, p->n, ps.s, ps.r, base, stride, inverse, st),
+                 "strike pass");
+        std::swap(cur, nxt);
+        ++pi;
+      }
+    }
+    if (inverse) TFFT_TRY(launch_scale(p->prec, cur, rows * p->n, 1.0 / (double)p->n, st), "strike scale");
+    TFFT_TRY((int)cudaMemcpyAsync((char*)y + a * p->n * cb, cur, rows * p->n * cb, cudaMemcpyDeviceToDevice, st),
+             "strike copy-out");
+    if (touched_rows) {
+      touched_rows->push_back(a);
+      touched_rows->push_back(b);
+    }
+  }
+  return 0;
+}
+
+int zero_counters(tfft_plan* p, uint64_t*& counters, cudaStream_t st) {
+  if (!counters) {
+    int e = p->counters.ensure(4 * sizeof(uint64_t));
+    if (e) return cuda_fail(e, "counters");
+    counters = (uint64_t*)p->counters.p;
+  }
+  TFFT_TRY((int)cudaMemsetAsync(counters, 0, 4 * sizeof(uint64_t), st), "counters memset");
+  return 0;
+}
+
+int split_faults(tfft_plan* p, const tfft_fault* faults, int nfaults, int64_t signal_offset, int64_t batch,
+                 std::vector<DevFault>& dev, std::vector<tfft_fault>& slow, bool k3_split_ok) {
+  for (int i = 0; i < nfaults; ++i) {
+    const tfft_fault& f = faults[i];
+    const int64_t r = f.signal - signal_offset;
+    if (r < 0 || r >= batch) continue;
+    if (f.element < 0 || f.element >= p->n || f.stage < 0 || f.stage >= (int)p->spans.size() || f.bit < 0 ||
+        f.bit >= (p->prec == 0 ? 32 : 64) || (f.part != 0 && f.part != 1))
+      return fail(TFFT_EINVAL, "fault spec out of range");
+    const bool in_kernel = f.stage == 0 || (k3_split_ok && f.stage == 1 && !p->k1 && k3_strikes_stage1(p->k3));
+    if (in_kernel) dev.push_back({r, f.element, f.stage, f.part, f.bit, 0});
+    else slow.push_back(f);
+  }
+  return 0;
+}
+
+int upload_faults(tfft_plan* p, const std::vector<DevFault>& dev, cudaStream_t st) {
+  if (dev.empty()) return 0;
+  int e = p->faults.ensure(dev.size() * sizeof(DevFault));
+  if (e) return cuda_fail(e, "fault buffer");
+  TFFT_TRY((int)cudaMemcpyAsync(p->faults.p, dev.data(), dev.size() * sizeof(DevFault), cudaMemcpyHostToDevice, st),
+           "fault upload");
+  return 0;
+}
+
+int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, int64_t signal_offset,
+              const std::vector<DevFault>& dev, uint64_t* counters, cudaStream_t st) {
+  if (p->k1) {
+    K1Args a{};
+    a.x = x;
+    a.y = y;
+    a.batch = batch;
+    a.weight0 = signal_offset;
+    a.tw = inverse ? p->tw_inv.p : p->tw_fwd.p;
+    a.faults = (const DevFault*)p->faults.p;
+    a.nfaults = (int)dev.size();
+    a.counters = (Counters*)counters;
+    TFFT_TRY(launch_k1(p->prec, p->logn, inverse != 0, false, a, p->num_sms, st), "k1 launch");
+    return 0;
+  }
+  int rc = k3_execute(p->k3, x, y, batch, inverse, (const DevFault*)p->faults.p, (int)dev.size(), (Counters*)counters,
+                      nullptr, st);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  return rc ? cuda_fail(rc, "k3 launch") : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tfft_version(void) { return 1; }
+const char* tfft_last_error(void) { return g_err.c_str(); }
+uint64_t tfft_launch_count(void) { return g_launches.load(); }
+
+int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans, const int32_t* radices,
+                     int64_t bs, tfft_plan** out) {
+  if (!out) return fail(TFFT_EINVAL, "null plan out-pointer");
+  *out = nullptr;
+  if (precision != 0 && precision != 1) return fail(TFFT_EINVAL, "precision must be 0 (single) or 1 (double)");
+  if (!is_pow2(n) || n < 2 || n > (int64_t(1) << 29)) return fail(TFFT_EINVAL, "n must be a power of two in [2, 2^29]");
+  if (nstages < 1 || nstages > 3 || bs < 1) return fail(TFFT_EINVAL, "plans have 1..3 stages and bs >= 1");
+  int64_t prod = 1;
+  for (int i = 0; i < nstages; ++i) {
+    if (!is_pow2(spans[i]) || spans[i] < 2) return fail(TFFT_EINVAL, "stage span must be a power of two >= 2");
+    if (!is_pow2(radices[i]) || radices[i] < 2 || radices[i] > 32 || radices[i] > spans[i])
+      return fail(TFFT_EINVAL, "invalid micro radix");
+    prod *= spans[i];
+  }
+  if (prod != n) return fail(TFFT_EINVAL, "stage spans do not multiply to n");
+  tfft_plan* p = new tfft_plan();
+  p->n = n;
+  p->logn = ilog2_64(n);
+  p->prec = precision;
+  p->bs = bs;
+  p->spans.assign(spans, spans + nstages);
+  p->radices.assign(radices, radices + nstages);
+  lower(p);
+  cudaGetDevice(&p->device);
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+  p->k1 = k1_supported(precision, p->logn) != 0;
+  if (p->k1) {
+    std::vector<long double> re, im;
+    fill_twiddles(re, im, n);
+    int e = 0;
+    if (precision == 0) {
+      std::vector<float> f, fi;
+      pack(re, im, false, f);
+      pack(re, im, true, fi);
+      e = upload(p->tw_fwd, f.data(), f.size() * 4);
+      if (!e) e = upload(p->tw_inv, fi.data(), fi.size() * 4);
+    } else {
+      std::vector<double> d, di;
+      pack(re, im, false, d);
+      pack(re, im, true, di);
+      e = upload(p->tw_fwd, d.data(), d.size() * 8);
+      if (!e) e = upload(p->tw_inv, di.data(), di.size() * 8);
+    }
+    if (e) {
+      tfft_plan_destroy(p);
+      return cuda_fail(e, "twiddle upload");
+    }
+  } else {
+    int rc = k3_create(n, precision, p->spans.data(), (int)p->spans.size(), p->num_sms, &p->k3);
+    if (rc) {
+      std::string msg = g_err.empty() ? std::string("k3 plan") : g_err;
+      tfft_plan_destroy(p);
+      return rc == (int)cudaErrorInvalidValue ? fail(TFFT_EUNSUPPORTED, "unsupported size for the two-pass kernel")
+                                              : cuda_fail(rc, "k3 plan");
+    }
+  }
+  *out = p;
+  return TFFT_OK;
+}
+
+int tfft_plan_destroy(tfft_plan* p) {
+  if (!p) return TFFT_OK;
+  DevBuf* all[] = {&p->tw_fwd, &p->tw_inv, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
+                   &p->ws, &p->win_count, &p->scratch_a, &p->scratch_b, &p->base, &p->col_a, &p->col_b, &p->col64};
+  for (DevBuf* b : all) b->release();
+  if (p->k3) k3_destroy(p->k3);
+  if (p->promoted) tfft_plan_destroy(p->promoted);
+  delete p;
+  return TFFT_OK;
+}
+
+int tfft_execute(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, int64_t signal_offset,
+                 const tfft_fault* faults, int nfaults, uint64_t* counters, void* stream) {
+  if (!p || !x || !y || batch < 1) return fail(TFFT_EINVAL, "invalid execute arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = zero_counters(p, counters, st);
+  if (rc) return rc;
+  std::vector<DevFault> dev;
+  std::vector<tfft_fault> slow;
+  rc = split_faults(p, faults, nfaults, signal_offset, batch, dev, slow, true);
+  if (rc) return rc;
+  rc = upload_faults(p, dev, st);
+  if (rc) return rc;
+  rc = run_plain(p, x, y, batch, inverse, signal_offset, dev, counters, st);
+  if (rc) return rc;
+  if (!slow.empty()) return strike_path(p, x, y, batch, inverse, signal_offset, slow, st, nullptr);
+  return TFFT_OK;
+}
+
+int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t signal_offset, int enc,
+                   double delta, int64_t T, const tfft_fault* faults, int nfaults, const tfft_sums* sums,
+                   uint64_t* counters, void* stream) {
+  if (!p || !x || !y || batch < 1 || !sums || T < 1 || enc < 0 || enc > 2 || !(delta > 0))
+    return fail(TFFT_EINVAL, "invalid protected arguments");
+  const int64_t W = T * p->bs;
+  if (signal_offset % W) return fail(TFFT_EINVAL, "signal_offset must be a multiple of group_size * bs");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = zero_counters(p, counters, st);
+  if (rc) return rc;
+  rc = ensure_row(p, enc);
+  if (rc) return rc;
+  std::vector<DevFault> dev;
+  std::vector<tfft_fault> slow;
+  rc = split_faults(p, faults, nfaults, signal_offset, batch, dev, slow, true);
+  if (rc) return rc;
+  rc = upload_faults(p, dev, st);
+  if (rc) return rc;
+  const int64_t ntx = (batch + p->bs - 1) / p->bs;
+  const int64_t nwin = (ntx + T - 1) / T;
+  AbftArgs ab{};
+  ab.row = p->rows[enc].p;
+  ab.enc = enc;
+  ab.delta = delta;
+  ab.c_in = sums->c_in;
+  ab.c_out = sums->c_out;
+  ab.floors = sums->floors;
+  ab.div = sums->div;
+  ab.win_div = sums->win_div;
+  ab.win_signals = W;
+  ab.nwin = nwin;
+  if (p->k1) {
+    const int spt = k1_slots(p->prec, p->logn);
+    if (W <= 4) {
+      ab.mode = 0;
+      ab.pieces = 1;
+    } else {
+      ab.mode = 1;
+      const int64_t piece = (int64_t)spt * 16;
+      ab.pieces = (W + piece - 1) / piece;
+    }
+    if (ab.mode == 1 && ab.pieces > 1) {
+      int e = p->ws.ensure((size_t)nwin * ab.pieces * 2 * p->n * cbytes(p->prec));
+      if (e) return cuda_fail(e, "abft workspace");
+      const size_t cnt_bytes = (size_t)nwin * sizeof(unsigned);
+      if (p->win_count.cap < cnt_bytes) {
+        e = p->win_count.ensure(cnt_bytes);
+        if (e) return cuda_fail(e, "window counters");
+        TFFT_TRY((int)cudaMemsetAsync(p->win_count.p, 0, p->win_count.cap, st), "window counter memset");
+      }
+      ab.ws = p->ws.p;
+      ab.win_count = (unsigned*)p->win_count.p;
+    }
+    K1Args a{};
+    a.x = x;
+    a.y = y;
+    a.batch = batch;
+    a.weight0 = signal_offset;
+    a.tw = p->tw_fwd.p;
+    a.faults = (const DevFault*)p->faults.p;
+    a.nfaults = (int)dev.size();
+    a.counters = (Counters*)counters;
+    a.abft = ab;
+    TFFT_TRY(launch_k1(p->prec, p->logn, false, true, a, p->num_sms, st), "k1 abft launch");
+  } else {
+    int e = k3_protected(p->k3, x, y, batch, signal_offset, (const DevFault*)p->faults.p, (int)dev.size(),
+                         (Counters*)counters, ab, p->rows[enc].p, st);
+    g_launches.fetch_add(3, std::memory_order_relaxed);
+    if (e) return cuda_fail(e, "k3 abft launch");
+  }
+  if (slow.empty()) return TFFT_OK;
+  // strike path for the faults the fused kernel cannot reach, then refresh
+  // the affected rows' checksums and their windows' group divergences
+  std::vector<int64_t> touched;
+  rc = strike_path(p, x, y, batch, 0, signal_offset, slow, st, &touched);
+  if (rc) return rc;
+  const size_t cb = cbytes(p->prec);
+  for (size_t i = 0; i < touched.size(); i += 2) {
+    const int64_t a = touched[i], b = touched[i + 1];
+    TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, a, b - a, p->rows[enc].p,
+                                  p->k1 ? p->tw_fwd.p : k3_enc_table(p->k3), enc, delta, ab, (Counters*)counters, 1, st),
+             "strike row checksums");
+    const int64_t w = a / W;
+    const int64_t w0 = w * W, w1 = std::min<int64_t>(w0 + W, batch);
+    int e = p->col_a.ensure(p->n * cb);
+    if (!e) e = p->col_b.ensure(p->n * cb);
+    if (!e) e = p->col64.ensure(p->n * cb);
+    if (e) return cuda_fail(e, "window columns");
+    TFFT_TRY(launch_weighted_cols(p->prec, x, p->n, w0, w1, W, signal_offset, p->col_a.p, st), "window s_in");
+    TFFT_TRY(launch_weighted_cols(p->prec, y, p->n, w0, w1, W, signal_offset, p->col_b.p, st), "window s_out");
+    std::vector<DevFault> none;
+    uint64_t* c2 = nullptr;
+    int e2 = p->counters.ensure(8 * sizeof(uint64_t));
+    if (e2) return cuda_fail(e2, "counters");
+    c2 = (uint64_t*)p->counters.p + 4;
+    rc = run_plain(p, p->col_a.p, p->col64.p, 1, 0, 0, none, c2, st);
+    if (rc) return rc;
+    TFFT_TRY(launch_group_div(p->prec, p->col64.p, p->col_b.p, p->n, sums->win_div + w, st), "window group div");
+  }
+  return TFFT_OK;
+}
+
+int tfft_stockham_pass(const void* src, void* dst, int64_t rows, int64_t n, int64_t s, int r, const void* base,
+                       int inverse, int precision, void* stream) {
+  if (!src || !dst || !base || rows < 1 || n < 2 || s < 1 || (r != 2 && r != 4) || n % (s * r))
+    return fail(TFFT_EINVAL, r != 2 && r != 4 ? "kernel supports radix 2 and 4" : "invalid stockham_pass arguments");
+  TFFT_TRY(launch_stockham_pass(precision, src, dst, rows, n, s, r, base, 1, inverse, (cudaStream_t)stream),
+           "stockham_pass");
+  return TFFT_OK;
+}
+
+int tfft_left_row(int enc, int64_t n, int precision, void* out_host) {
+  if (!out_host || n < 1 || enc < 0 || enc > 2 || (precision != 0 && precision != 1))
+    return fail(TFFT_EINVAL, "invalid left-row arguments");
+  std::vector<long double> re(n, 0.0L), im(n, 0.0L);
+  if (enc == ENC_ONES) {
+    re[0] = (long double)n;
+  } else if (enc == ENC_JOU) {
+    re[n - 1] = (long double)n;
+  } else {
+    // row[j] = (1 - w3^n) / (1 - w3 w_n^j), w3 = e^{-2 pi i/3}; the pole phase
+    // (1/3 + j/n) is reduced exactly as the integer m = (n + 3j) mod 3n
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    const int64_t nm3 = n % 3;
+    const long double a = two_pi * (long double)nm3 / 3.0L;  // w3^n = e^{-i a}
+    const long double num_re = 1.0L - cosl(a), num_im = sinl(a);
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t m = (n + 3 * j) % (3 * n);
+      const long double th = two_pi * (long double)m / (3.0L * (long double)n);
+      const long double sh = sinl(th / 2);
+      const long double den_re = 2.0L * sh * sh, den_im = sinl(th);  // 1 - e^{-i th}
+      const long double dd = den_re * den_re + den_im * den_im;
+      re[j] = (num_re * den_re + num_im * den_im) / dd;
+      im[j] = (num_im * den_re - num_re * den_im) / dd;
+    }
+  }
+  if (precision == 0) {
+    float* o = (float*)out_host;
+    for (int64_t j = 0; j < n; ++j) {
+      o[2 * j] = (float)re[j];
+      o[2 * j + 1] = (float)im[j];
+    }
+  } else {
+    double* o = (double*)out_host;
+    for (int64_t j = 0; j < n; ++j) {
+      o[2 * j] = (double)re[j];
+      o[2 * j + 1] = (double)im[j];
+    }
+  }
+  return TFFT_OK;
+}
+
+int tfft_weighted_columns(int precision, const void* src, int64_t n, int64_t row0, int64_t row1, int64_t group,
+                          int64_t weight0, void* out, void* stream) {
+  if (!src || !out || row1 < row0 || group < 1) return fail(TFFT_EINVAL, "invalid weighted_columns arguments");
+  TFFT_TRY(launch_weighted_cols(precision, src, n, row0, row1, group, weight0, out, (cudaStream_t)stream),
+           "weighted columns");
+  return TFFT_OK;
+}
+
+int tfft_vec_add(int precision, void* a, const void* b, int64_t n, void* stream) {
+  TFFT_TRY(launch_vadd(precision, a, b, n, (cudaStream_t)stream), "vec add");
+  return TFFT_OK;
+}
+
+int tfft_vec_axpby(int precision, void* z, int64_t n, double ar, double ai, const void* x, double br, double bi,
+                   const void* y, void* stream) {
+  TFFT_TRY(launch_axpby(precision, z, n, ar, ai, x, br, bi, y, (cudaStream_t)stream), "axpby");
+  return TFFT_OK;
+}
+
+int tfft_group_divergence(int precision, const void* ref, const void* s_out, int64_t n, double* out_dev,
+                          void* stream) {
+  TFFT_TRY(launch_group_div(precision, ref, s_out, n, out_dev, (cudaStream_t)stream), "group divergence");
+  return TFFT_OK;
+}
+
+int tfft_correction_column(tfft_plan* p, const void* snap_in, const void* snap_out, double weight, void* col,
+                           double* res_dev, void* stream) {
+  if (!p) return fail(TFFT_EINVAL, "null plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  tfft_plan* p64 = p;
+  const void* in64 = snap_in;
+  if (p->prec == 0) {
+    if (!p->promoted) {
+      int rc = tfft_plan_create(p->n, 1, (int)p->spans.size(), p->spans.data(), p->radices.data(), p->bs, &p->promoted);
+      if (rc) return rc;
+    }
+    p64 = p->promoted;
+    int e = p->col64.ensure(p->n * 16);
+    if (e) return cuda_fail(e, "promote buffer");
+    TFFT_TRY(launch_promote(snap_in, p->col64.p, p->n, st), "promote");
+    in64 = p->col64.p;
+  }
+  int e = p64->col_a.ensure(p->n * 16);
+  if (e) return cuda_fail(e, "ref buffer");
+  std::vector<DevFault> none;
+  int e2 = p64->counters.ensure(8 * sizeof(uint64_t));
+  if (e2) return cuda_fail(e2, "counters");
+  int rc = run_plain(p64, in64, p64->col_a.p, 1, 0, 0, none, (uint64_t*)p64->counters.p + 4, st);
+  if (rc) return rc;
+  TFFT_TRY(launch_correction_column(p->prec, snap_out, p64->col_a.p, p->n, weight, col, res_dev, st),
+           "correction column");
+  return TFFT_OK;
+}
+
+int tfft_patch_row(tfft_plan* p, void* y_row, const void* col, int enc, double* res_dev, void* stream) {
+  if (!p) return fail(TFFT_EINVAL, "null plan");
+  TFFT_TRY(launch_patch_row(p->prec, y_row, col, p->n, enc, p->k1 ? p->tw_fwd.p : k3_enc_table(p->k3), res_dev,
+                            (cudaStream_t)stream),
+           "patch row");
+  return TFFT_OK;
+}
+
+int tfft_row_checksums(tfft_plan* p, const void* x, const void* y, int64_t row0, int64_t nrows, int enc,
+                       double delta, const tfft_sums* sums, uint64_t* counters, int count, void* stream) {
+  if (!p || !sums) return fail(TFFT_EINVAL, "invalid row_checksums arguments");
+  int rc = ensure_row(p, enc);
+  if (rc) return rc;
+  AbftArgs ab{};
+  ab.c_in = sums->c_in;
+  ab.c_out = sums->c_out;
+  ab.floors = sums->floors;
+  ab.div = sums->div;
+  if (!counters) {
+    int e = p->counters.ensure(8 * sizeof(uint64_t));
+    if (e) return cuda_fail(e, "counters");
+    counters = (uint64_t*)p->counters.p;
+  }
+  TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, row0, nrows, p->rows[enc].p,
+                                p->k1 ? p->tw_fwd.p : k3_enc_table(p->k3), enc, delta, ab, (Counters*)counters, count,
+                                (cudaStream_t)stream),
+           "row checksums");
+  return TFFT_OK;
+}
+
+int tfft_jou_variant(tfft_plan* p, const void* x, void* out, int64_t rows, void* stream) {
+  if (!p) return fail(TFFT_EINVAL, "null plan");
+  TFFT_TRY(launch_jou(p->prec, 0, x, out, rows, p->n, nullptr, (cudaStream_t)stream), "jou variant");
+  return TFFT_OK;
+}
+
+int tfft_jou_undo(tfft_plan* p, void* y, int64_t rows, void* stream) {
+  if (!p) return fail(TFFT_EINVAL, "null plan");
+  const void* twi = p->k1 ? p->tw_inv.p : k3_enc_table_inv(p->k3);
+  TFFT_TRY(launch_jou(p->prec, 1, nullptr, y, rows, p->n, twi, (cudaStream_t)stream), "jou undo");
+  return TFFT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,451 @@
+// Rare-path and boundary kernels.
+//
+//  * stockham_pass  — one radix-2/4 DIT Stockham pass over a row block with the
+//    reference's exact index contract and twiddle arithmetic (w^2 = w*w,
+//    w^3 = w^2*w; _kernels.pyx:38-71). It backs the plugin-boundary
+//    `stockham_pass` entry point and the stage-strike path, which replays a
+//    faulted transaction pass by pass so stage-k strikes hit the canonical
+//    intermediate exactly where the reference's injector does (fft_core.py:271).
+//  * flip_element   — the strike itself (fault.py:99-107).
+//  * row_checksums  — per-signal c_in / c_out / floor / divergence for a row
+//    range (abft.py:648-665); used after a strike-path rerun and on recompute.
+//  * weighted_cols  — per-transaction (or per-range) location-weighted columns
+//    sum_j w_j x_j (abft.py:668-677), accumulated in FP64.
+//  * vec ops, group divergence and the fused correction step (abft.py:297-330,
+//    392-418) for the replay engine.
+#include "tfft_common.cuh"
+#include "tfft_internal.h"
+#include "tfft_aux.h"
+
+namespace tfft {
+
+// ---------------------------------------------------------------------------
+
+template <typename T, bool INV>
+__global__ void stockham_pass_kernel(const C<T>* __restrict__ src, C<T>* __restrict__ dst, int64_t rows, int64_t n,
+                                     int64_t s, int r, const C<T>* __restrict__ base, int64_t base_stride) {
+  using CT = C<T>;
+  const int64_t nb = n / r;  // butterflies per row
+  const int64_t m = n / (s * r);
+  const int64_t total = rows * nb;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = id / nb;
+    const int64_t j = id - row * nb;  // j = p*s + q
+    const int64_t q = j % s, p = j / s;
+    const CT* in = src + row * n;
+    CT* out = dst + row * n;
+    const CT w = base[q * base_stride];
+    const int64_t sm = s * m;
+    const int64_t i0 = p * s + q;
+    if (r == 2) {
+      const CT u0 = in[i0];
+      const CT u1 = cmul<T>(in[i0 + sm], w);
+      out[2 * p * s + q] = cadd<T>(u0, u1);
+      out[2 * p * s + q + s] = csub<T>(u0, u1);
+    } else {
+      const CT w2 = cmul<T>(w, w);
+      const CT w3 = cmul<T>(w2, w);
+      const CT u0 = in[i0];
+      const CT u1 = cmul<T>(in[i0 + sm], w);
+      const CT u2 = cmul<T>(in[i0 + 2 * sm], w2);
+      const CT u3 = cmul<T>(in[i0 + 3 * sm], w3);
+      const CT A = cadd<T>(u0, u2), Bv = csub<T>(u0, u2);
+      const CT Cv = cadd<T>(u1, u3), D = rot90<T, INV>(csub<T>(u1, u3));
+      const int64_t o0 = 4 * p * s + q;
+      out[o0] = cadd<T>(A, Cv);
+      out[o0 + s] = cadd<T>(Bv, D);
+      out[o0 + 2 * s] = csub<T>(A, Cv);
+      out[o0 + 3 * s] = csub<T>(Bv, D);
+    }
+  }
+}
+
+int launch_stockham_pass(int prec, const void* src, void* dst, int64_t rows, int64_t n, int64_t s, int r,
+                         const void* base, int64_t base_stride, int inverse, cudaStream_t st) {
+  const int64_t total = rows * (n / r);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  if (prec == 0) {
+    if (inverse)
+      stockham_pass_kernel<float, true><<<(unsigned)blocks, 256, 0, st>>>((const float2*)src, (float2*)dst, rows, n, s, r,
+                                                                         (const float2*)base, base_stride);
+    else
+      stockham_pass_kernel<float, false><<<(unsigned)blocks, 256, 0, st>>>((const float2*)src, (float2*)dst, rows, n, s, r,
+                                                                          (const float2*)base, base_stride);
+  } else {
+    if (inverse)
+      stockham_pass_kernel<double, true><<<(unsigned)blocks, 256, 0, st>>>((const double2*)src, (double2*)dst, rows, n, s, r,
+                                                                          (const double2*)base, base_stride);
+    else
+      stockham_pass_kernel<double, false><<<(unsigned)blocks, 256, 0, st>>>((const double2*)src, (double2*)dst, rows, n, s,
+                                                                           r, (const double2*)base, base_stride);
+  }
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void flip_element_kernel(C<T>* buf, int64_t index, int part, int bit) {
+  C<T> v = buf[index];
+  if (part == 0) v.x = flip_bits(v.x, bit);
+  else v.y = flip_bits(v.y, bit);
+  buf[index] = v;
+}
+
+int launch_flip(int prec, void* buf, int64_t index, int part, int bit, cudaStream_t st) {
+  if (prec == 0) flip_element_kernel<float><<<1, 1, 0, st>>>((float2*)buf, index, part, bit);
+  else flip_element_kernel<double><<<1, 1, 0, st>>>((double2*)buf, index, part, bit);
+  return (int)cudaGetLastError();
+}
+
+template <typename T>
+__global__ void scale_kernel(C<T>* buf, int64_t count, T s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = cscale<T>(buf[i], s);
+}
+
+int launch_scale(int prec, void* buf, int64_t count, double s, cudaStream_t st) {
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (prec == 0) scale_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((float2*)buf, count, (float)s);
+  else scale_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((double2*)buf, count, s);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// block-wide deterministic FP64 sum (fixed tree), 256 threads
+
+template <int NV>
+__device__ __forceinline__ void block_sum256(double (&r)[NV], double* sh) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) r[k] += __shfl_xor_sync(0xffffffffu, r[k], off);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sh[w * NV + k] = r[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double acc = sh[k];
+      for (int i = 1; i < 8; ++i) acc += sh[i * NV + k];
+      r[k] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ C<T> enc_value(int enc, int64_t k, int64_t n, const C<T>* tw) {
+  if (enc == ENC_WANG) {
+    const int m = (int)(k % 3);
+    const T h = (T)0.86602540378443864676372317075294;
+    return m == 0 ? mk<T>(1, 0) : (m == 1 ? mk<T>((T)-0.5, -h) : mk<T>((T)-0.5, h));
+  }
+  if (enc == ENC_ONES) return mk<T>(1, 0);
+  return tw[k];
+}
+
+// one CTA per signal row: c_in, c_out, floor, div; bumps the counters
+template <typename T>
+__global__ void __launch_bounds__(256) row_checksums_kernel(const C<T>* __restrict__ x, const C<T>* __restrict__ y,
+                                                            int64_t n, int64_t row0, const C<T>* __restrict__ row,
+                                                            const C<T>* __restrict__ tw, int enc, double delta,
+                                                            double* c_in, double* c_out, double* floors, double* div,
+                                                            Counters* counters, int count) {
+  __shared__ double sh[8 * 5];
+  const int64_t r = row0 + blockIdx.x;
+  const C<T>* xr = x + r * n;
+  const C<T>* yr = y + r * n;
+  C<T> ci = mk<T>(0, 0), co = mk<T>(0, 0);
+  T fl = 0;
+  for (int64_t k = threadIdx.x; k < n; k += 256) {
+    const C<T> xv = xr[k], yv = yr[k];
+    ci = cadd<T>(ci, cmul<T>(row[k], xv));
+    fl = rfma(xv.x, xv.x, rfma(xv.y, xv.y, fl));
+    co = cadd<T>(co, cmul<T>(enc_value<T>(enc, k, n, tw), yv));
+  }
+  double acc[5] = {(double)ci.x, (double)ci.y, (double)fl, (double)co.x, (double)co.y};
+  block_sum256<5>(acc, sh);
+  if (threadIdx.x == 0) {
+    const double floor_v = sqrt(acc[2]) / sqrt((double)n);
+    double dv;
+    if (!isfinite(acc[3]) || !isfinite(acc[4])) dv = __longlong_as_double(0x7ff0000000000000ll);
+    else dv = hypot(acc[0] - acc[3], acc[1] - acc[4]) / fmax(fmax(hypot(acc[0], acc[1]), floor_v), 1e-30);
+    c_in[2 * r] = acc[0];
+    c_in[2 * r + 1] = acc[1];
+    c_out[2 * r] = acc[3];
+    c_out[2 * r + 1] = acc[4];
+    floors[r] = floor_v;
+    div[r] = dv;
+    if (count) {
+      if (dv > delta) atomicAdd(&counters->triggered, 1ull);
+      atomicMax(&counters->max_div_bits, (unsigned long long)__double_as_longlong(dv));
+    }
+  }
+}
+
+int launch_row_checksums(int prec, const void* x, const void* y, int64_t n, int64_t row0, int64_t nrows,
+                         const void* row, const void* tw, int enc, double delta, const AbftArgs& ab, Counters* counters,
+                         int count, cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  if (prec == 0)
+    row_checksums_kernel<float><<<(unsigned)nrows, 256, 0, st>>>((const float2*)x, (const float2*)y, n, row0,
+                                                                (const float2*)row, (const float2*)tw, enc, delta,
+                                                                ab.c_in, ab.c_out, ab.floors, ab.div, counters, count);
+  else
+    row_checksums_kernel<double><<<(unsigned)nrows, 256, 0, st>>>((const double2*)x, (const double2*)y, n, row0,
+                                                                 (const double2*)row, (const double2*)tw, enc, delta,
+                                                                 ab.c_in, ab.c_out, ab.floors, ab.div, counters, count);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// weighted column sums: out[g][k] = sum_{j in group g} (weight0 + j + 1) * src[j][k]
+// groups are consecutive row ranges of `gsize` rows starting at row0 (last short)
+
+template <typename T>
+__global__ void weighted_cols_kernel(const C<T>* __restrict__ src, int64_t n, int64_t row0, int64_t row1,
+                                     int64_t gsize, int64_t weight0, C<T>* __restrict__ out) {
+  const int64_t ngroups = (row1 - row0 + gsize - 1) / gsize;
+  const int64_t total = ngroups * n;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gidx = id / n, k = id - gidx * n;
+    const int64_t a = row0 + gidx * gsize, b = min(a + gsize, row1);
+    double re = 0, im = 0;
+    for (int64_t j = a; j < b; ++j) {
+      const C<T> v = src[j * n + k];
+      const double w = (double)(weight0 + j + 1);
+      re = fma(w, (double)v.x, re);
+      im = fma(w, (double)v.y, im);
+    }
+    out[id] = mk<T>((T)re, (T)im);
+  }
+}
+
+int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int64_t row1, int64_t gsize,
+                         int64_t weight0, void* out, cudaStream_t st) {
+  const int64_t ngroups = (row1 - row0 + gsize - 1) / gsize;
+  int64_t blocks = (ngroups * n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) return 0;
+  if (prec == 0)
+    weighted_cols_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float2*)src, n, row0, row1, gsize, weight0,
+                                                                 (float2*)out);
+  else
+    weighted_cols_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double2*)src, n, row0, row1, gsize, weight0,
+                                                                  (double2*)out);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// z = a*x + b*y (complex scalars a, b given in FP64; x or y may be null)
+
+template <typename T>
+__global__ void axpby_kernel(C<T>* z, int64_t n, double ar, double ai, const C<T>* x, double br, double bi,
+                             const C<T>* y) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    C<T> acc = mk<T>(0, 0);
+    if (x) acc = cadd<T>(acc, cmul<T>(mk<T>((T)ar, (T)ai), x[k]));
+    if (y) acc = cadd<T>(acc, cmul<T>(mk<T>((T)br, (T)bi), y[k]));
+    z[k] = acc;
+  }
+}
+
+int launch_axpby(int prec, void* z, int64_t n, double ar, double ai, const void* x, double br, double bi,
+                 const void* y, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) return 0;
+  if (prec == 0)
+    axpby_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((float2*)z, n, ar, ai, (const float2*)x, br, bi,
+                                                         (const float2*)y);
+  else
+    axpby_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((double2*)z, n, ar, ai, (const double2*)x, br, bi,
+                                                          (const double2*)y);
+  return (int)cudaGetLastError();
+}
+
+// plain sum a = a + b in working precision (the replay's s_in += t_in)
+template <typename T>
+__global__ void vadd_kernel(C<T>* a, const C<T>* b, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    a[k] = cadd<T>(a[k], b[k]);
+}
+
+int launch_vadd(int prec, void* a, const void* b, int64_t n, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) return 0;
+  if (prec == 0) vadd_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((float2*)a, (const float2*)b, n);
+  else vadd_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((double2*)a, (const double2*)b, n);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// group divergence ||ref - s_out||_2 / max(||ref||_2, 1e-30) (abft.py:502-507)
+
+template <typename T>
+__global__ void __launch_bounds__(256) group_div_kernel(const C<T>* ref, const C<T>* s_out, int64_t n, double* out) {
+  __shared__ double sh[8 * 2];
+  double acc[2] = {0, 0};
+  for (int64_t k = threadIdx.x; k < n; k += 256) {
+    const double dr = (double)ref[k].x - (double)s_out[k].x;
+    const double di = (double)ref[k].y - (double)s_out[k].y;
+    acc[0] += dr * dr + di * di;
+    acc[1] += (double)ref[k].x * (double)ref[k].x + (double)ref[k].y * (double)ref[k].y;
+  }
+  block_sum256<2>(acc, sh);
+  if (threadIdx.x == 0) *out = sqrt(acc[0]) / fmax(sqrt(acc[1]), 1e-30);
+}
+
+int launch_group_div(int prec, const void* ref, const void* s_out, int64_t n, double* out, cudaStream_t st) {
+  if (prec == 0) group_div_kernel<float><<<1, 256, 0, st>>>((const float2*)ref, (const float2*)s_out, n, out);
+  else group_div_kernel<double><<<1, 256, 0, st>>>((const double2*)ref, (const double2*)s_out, n, out);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// correction column (abft.py:297-330): col = (snap_out - ref64) / w_k, formed in
+// FP64 (ref64 is the FP64 transform of the snapshot input), cast to working
+// precision; report finiteness and max|col| so the host applies the usability
+// rule. Then, if asked, patch y_k -= col and re-form c_out = y_k . enc.
+// res: [0] all finite (1/0), [1] max |col|, [2] c_out re, [3] c_out im
+
+template <typename T>
+__global__ void __launch_bounds__(256) correction_column_kernel(const C<T>* snap_out, const double2* ref64, int64_t n,
+                                                                double weight, C<T>* col, double* res) {
+  __shared__ double sh[8 * 2];
+  double acc[2] = {0, 0};  // [0] non-finite count, [1] max |col|
+  for (int64_t k = threadIdx.x; k < n; k += 256) {
+    const double re = ((double)snap_out[k].x - ref64[k].x) / weight;
+    const double im = ((double)snap_out[k].y - ref64[k].y) / weight;
+    const C<T> c = mk<T>((T)re, (T)im);
+    col[k] = c;
+    if (!isfinite((double)c.x) || !isfinite((double)c.y)) acc[0] += 1.0;
+    else acc[1] = fmax(acc[1], hypot((double)c.x, (double)c.y));
+  }
+  // max-reduction (order independent) for acc[1]; sum for acc[0]
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+    acc[1] = fmax(acc[1], __shfl_xor_sync(0xffffffffu, acc[1], off));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sh[w * 2] = acc[0];
+    sh[w * 2 + 1] = acc[1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bad = 0, mx = 0;
+    for (int i = 0; i < 8; ++i) {
+      bad += sh[2 * i];
+      mx = fmax(mx, sh[2 * i + 1]);
+    }
+    res[0] = bad == 0 ? 1.0 : 0.0;
+    res[1] = mx;
+  }
+}
+
+// FP64 data: the reference subtracts in working precision (abft.py:315-317);
+// the column is (snap_out - ref) / w with ref in the same precision.
+int launch_correction_column(int prec, const void* snap_out, const void* ref64, int64_t n, double weight, void* col,
+                             double* res, cudaStream_t st) {
+  if (prec == 0)
+    correction_column_kernel<float><<<1, 256, 0, st>>>((const float2*)snap_out, (const double2*)ref64, n, weight,
+                                                      (float2*)col, res);
+  else
+    correction_column_kernel<double><<<1, 256, 0, st>>>((const double2*)snap_out, (const double2*)ref64, n, weight,
+                                                       (double2*)col, res);
+  return (int)cudaGetLastError();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) patch_row_kernel(C<T>* yk, const C<T>* col, int64_t n, int enc,
+                                                        const C<T>* tw, double* res) {
+  __shared__ double sh[8 * 2];
+  C<T> co = mk<T>(0, 0);
+  for (int64_t k = threadIdx.x; k < n; k += 256) {
+    const C<T> v = csub<T>(yk[k], col[k]);
+    yk[k] = v;
+    co = cadd<T>(co, cmul<T>(enc_value<T>(enc, k, n, tw), v));
+  }
+  double acc[2] = {(double)co.x, (double)co.y};
+  block_sum256<2>(acc, sh);
+  if (threadIdx.x == 0) {
+    res[2] = acc[0];
+    res[3] = acc[1];
+  }
+}
+
+int launch_patch_row(int prec, void* yk, const void* col, int64_t n, int enc, const void* tw, double* res,
+                     cudaStream_t st) {
+  if (prec == 0)
+    patch_row_kernel<float><<<1, 256, 0, st>>>((float2*)yk, (const float2*)col, n, enc, (const float2*)tw, res);
+  else
+    patch_row_kernel<double><<<1, 256, 0, st>>>((double2*)yk, (const double2*)col, n, enc, (const double2*)tw, res);
+  return (int)cudaGetLastError();
+}
+
+// promote / demote a column between working precision and FP64
+__global__ void promote_kernel(const float2* in, double2* out, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = make_double2(in[k].x, in[k].y);
+}
+
+int launch_promote(const void* in, void* out, int64_t n, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) return 0;
+  promote_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float2*)in, (double2*)out, n);
+  return (int)cudaGetLastError();
+}
+
+// Jou encoding input variant x' = 2 x_k + x_{k+1 mod n} (abft.py:333-334) and
+// its undo y /= (2 + e^{2 pi i j / n}) (abft.py:337-339)
+template <typename T>
+__global__ void jou_variant_kernel(const C<T>* x, C<T>* out, int64_t rows, int64_t n) {
+  const int64_t total = rows * n;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = id / n, k = id - r * n;
+    const C<T> a = x[id], b = x[r * n + (k + 1 == n ? 0 : k + 1)];
+    out[id] = cadd<T>(cscale<T>(a, (T)2), b);
+  }
+}
+
+template <typename T>
+__global__ void jou_undo_kernel(C<T>* y, int64_t rows, int64_t n, const C<T>* tw_inv) {
+  const int64_t total = rows * n;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = id % n;
+    const C<T> w = tw_inv[k];  // e^{+2 pi i k / n}
+    const double dr = 2.0 + (double)w.x, di = (double)w.y;
+    const double den = dr * dr + di * di;
+    const C<T> v = y[id];
+    const double re = ((double)v.x * dr + (double)v.y * di) / den;
+    const double im = ((double)v.y * dr - (double)v.x * di) / den;
+    y[id] = mk<T>((T)re, (T)im);
+  }
+}
+
+int launch_jou(int prec, int undo, const void* x, void* out, int64_t rows, int64_t n, const void* tw_inv,
+               cudaStream_t st) {
+  int64_t blocks = (rows * n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) return 0;
+  if (prec == 0) {
+    if (undo) jou_undo_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((float2*)out, rows, n, (const float2*)tw_inv);
+    else jou_variant_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float2*)x, (float2*)out, rows, n);
+  } else {
+    if (undo) jou_undo_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((double2*)out, rows, n, (const double2*)tw_inv);
+    else jou_variant_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double2*)x, (double2*)out, rows, n);
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace tfft

@@ -1,0 +1,32 @@
+// Launchers for the rare-path / boundary kernels in tfft_aux.cu (library-private).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tfft_internal.h"
+
+namespace tfft {
+
+int launch_stockham_pass(int prec, const void* src, void* dst, int64_t rows, int64_t n, int64_t s, int r,
+                         const void* base, int64_t base_stride, int inverse, cudaStream_t st);
+int launch_flip(int prec, void* buf, int64_t index, int part, int bit, cudaStream_t st);
+int launch_scale(int prec, void* buf, int64_t count, double s, cudaStream_t st);
+int launch_row_checksums(int prec, const void* x, const void* y, int64_t n, int64_t row0, int64_t nrows,
+                         const void* row, const void* tw, int enc, double delta, const AbftArgs& ab, Counters* counters,
+                         int count, cudaStream_t st);
+int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int64_t row1, int64_t gsize,
+                         int64_t weight0, void* out, cudaStream_t st);
+int launch_axpby(int prec, void* z, int64_t n, double ar, double ai, const void* x, double br, double bi,
+                 const void* y, cudaStream_t st);
+int launch_vadd(int prec, void* a, const void* b, int64_t n, cudaStream_t st);
+int launch_group_div(int prec, const void* ref, const void* s_out, int64_t n, double* out, cudaStream_t st);
+int launch_correction_column(int prec, const void* snap_out, const void* ref64, int64_t n, double weight, void* col,
+                             double* res, cudaStream_t st);
+int launch_patch_row(int prec, void* yk, const void* col, int64_t n, int enc, const void* tw, double* res,
+                     cudaStream_t st);
+int launch_promote(const void* in, void* out, int64_t n, cudaStream_t st);
+int launch_jou(int prec, int undo, const void* x, void* out, int64_t rows, int64_t n, const void* tw_inv,
+               cudaStream_t st);
+
+}  // namespace tfft

@@ -1,0 +1,213 @@
+// Common device building blocks for the sm_100a batched FFT kernels.
+//
+// Every arithmetic op on signal data goes through the *_rn intrinsics below, so
+// nvcc never contracts across them: the plain kernels and their ABFT twins run
+// the identical instruction sequence on y, which is what makes a fault-free
+// run_protected bitwise equal to execute_plan (reference abft.py:694-696,
+// tests/test_abft.py:197-206).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tfft {
+
+template <typename T> struct cplx;
+template <> struct cplx<float> { using type = float2; };
+template <> struct cplx<double> { using type = double2; };
+template <typename T> using C = typename cplx<T>::type;
+
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float rfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <typename T> __device__ __forceinline__ C<T> mk(T re, T im) { C<T> r; r.x = re; r.y = im; return r; }
+template <typename T> __device__ __forceinline__ C<T> cadd(C<T> a, C<T> b) { return mk<T>(radd(a.x, b.x), radd(a.y, b.y)); }
+template <typename T> __device__ __forceinline__ C<T> csub(C<T> a, C<T> b) { return mk<T>(rsub(a.x, b.x), rsub(a.y, b.y)); }
+// (a.x b.x - a.y b.y, a.x b.y + a.y b.x) with one rounding on the fused term
+template <typename T> __device__ __forceinline__ C<T> cmul(C<T> a, C<T> b) {
+  return mk<T>(rfma(a.x, b.x, -rmul(a.y, b.y)), rfma(a.x, b.y, rmul(a.y, b.x)));
+}
+// multiply by -i (forward) or +i (inverse)
+template <typename T, bool INV> __device__ __forceinline__ C<T> rot90(C<T> a) {
+  return INV ? mk<T>(-a.y, a.x) : mk<T>(a.y, -a.x);
+}
+template <typename T> __device__ __forceinline__ C<T> cscale(C<T> a, T s) { return mk<T>(rmul(a.x, s), rmul(a.y, s)); }
+
+// ---------------------------------------------------------------------------
+// constant twiddles omega_R^k = exp(-+2 pi i k / R) for the in-register codelets
+
+template <typename T, int R, int K, bool INV>
+__device__ __forceinline__ C<T> wconst_mul(C<T> a) {
+  constexpr int k = ((K % R) + R) % R;
+  if constexpr (k == 0) {
+    return a;
+  } else if constexpr (4 * k == R) {
+    return rot90<T, INV>(a);
+  } else if constexpr (2 * k == R) {
+    return mk<T>(-a.x, -a.y);
+  } else if constexpr (4 * k == 3 * R) {
+    return rot90<T, !INV>(a);
+  } else if constexpr (8 * k == R || 8 * k == 3 * R || 8 * k == 5 * R || 8 * k == 7 * R) {
+    // (+-1 +- i)/sqrt2: two adds and two muls
+    const T h = (T)0.70710678118654752440084436210485;
+    // w = (cx + i sy) / sqrt2 with cx, sy in {+1, -1}
+    constexpr int cx = (8 * k == R || 8 * k == 7 * R) ? 1 : -1;
+    constexpr int sy0 = (8 * k == R || 8 * k == 3 * R) ? -1 : 1;  // forward sign
+    constexpr int sy = INV ? -sy0 : sy0;
+    // (a.x + i a.y)(cx + i sy) = (cx a.x - sy a.y) + i (sy a.x + cx a.y)
+    T re = (cx == 1) ? (sy == 1 ? rsub(a.x, a.y) : radd(a.x, a.y)) : (sy == 1 ? -radd(a.x, a.y) : rsub(a.y, a.x));
+    T im = (cx == 1) ? (sy == 1 ? radd(a.x, a.y) : rsub(a.y, a.x)) : (sy == 1 ? rsub(a.x, a.y) : -radd(a.x, a.y));
+    return mk<T>(rmul(re, h), rmul(im, h));
+  } else {
+    // remaining angles of the radix-16 codelet: k odd, omega_16^k = exp(-i pi k / 8)
+    static_assert(R == 16, "codelets stop at radix 16");
+    const T c1 = (T)0.92387953251128675612818318939678829;  // cos(pi/8)
+    const T s1 = (T)0.38268343236508977172845998403039887;  // sin(pi/8)
+    T c, s;  // forward omega = c + i s
+    if constexpr (k == 1) { c = c1; s = -s1; }
+    else if constexpr (k == 3) { c = s1; s = -c1; }
+    else if constexpr (k == 5) { c = -s1; s = -c1; }
+    else if constexpr (k == 7) { c = -c1; s = -s1; }
+    else if constexpr (k == 9) { c = -c1; s = s1; }
+    else if constexpr (k == 11) { c = -s1; s = c1; }
+    else if constexpr (k == 13) { c = s1; s = c1; }
+    else { c = c1; s = s1; }
+    if constexpr (INV) s = -s;
+    return cmul<T>(a, mk<T>(c, s));
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// in-register DFT codelets, natural order in and out (forward: omega = e^{-2 pi i/R})
+
+template <typename T, bool INV>
+__device__ __forceinline__ void dft2(C<T>& a0, C<T>& a1) {
+  C<T> t = a0;
+  a0 = cadd<T>(t, a1);
+  a1 = csub<T>(t, a1);
+}
+
+template <typename T, bool INV>
+__device__ __forceinline__ void dft4(C<T>& a0, C<T>& a1, C<T>& a2, C<T>& a3) {
+  C<T> A = cadd<T>(a0, a2), B = csub<T>(a0, a2);
+  C<T> Cc = cadd<T>(a1, a3), D = rot90<T, INV>(csub<T>(a1, a3));
+  a0 = cadd<T>(A, Cc);
+  a2 = csub<T>(A, Cc);
+  a1 = cadd<T>(B, D);
+  a3 = csub<T>(B, D);
+}
+
+template <typename T, int R, bool INV>
+__device__ __forceinline__ void dft(C<T>* a) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
+    dft2<T, INV>(a[0], a[1]);
+  } else if constexpr (R == 4) {
+    dft4<T, INV>(a[0], a[1], a[2], a[3]);
+  } else if constexpr (R == 8) {
+    dft4<T, INV>(a[0], a[2], a[4], a[6]);
+    dft4<T, INV>(a[1], a[3], a[5], a[7]);
+    a[3] = wconst_mul<T, 8, 1, INV>(a[3]);
+    a[5] = wconst_mul<T, 8, 2, INV>(a[5]);
+    a[7] = wconst_mul<T, 8, 3, INV>(a[7]);
+    // even half sits at a[0,2,4,6] (bins 0..3), odd half at a[1,3,5,7]
+    C<T> e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6];
+    C<T> o0 = a[1], o1 = a[3], o2 = a[5], o3 = a[7];
+    a[0] = cadd<T>(e0, o0); a[4] = csub<T>(e0, o0);
+    a[1] = cadd<T>(e1, o1); a[5] = csub<T>(e1, o1);
+    a[2] = cadd<T>(e2, o2); a[6] = csub<T>(e2, o2);
+    a[3] = cadd<T>(e3, o3); a[7] = csub<T>(e3, o3);
+  } else if constexpr (R == 16) {
+    // n = 4 n1 + n2; inner 4-point DFTs over n1, twiddle omega_16^{n2 k1}, outer over n2
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<T, INV>(a[n2], a[4 + n2], a[8 + n2], a[12 + n2]);
+    // a[4 k1 + n2] now holds B[n2][k1]
+    a[5] = wconst_mul<T, 16, 1, INV>(a[5]);
+    a[6] = wconst_mul<T, 16, 2, INV>(a[6]);
+    a[7] = wconst_mul<T, 16, 3, INV>(a[7]);
+    a[9] = wconst_mul<T, 16, 2, INV>(a[9]);
+    a[10] = wconst_mul<T, 16, 4, INV>(a[10]);
+    a[11] = wconst_mul<T, 16, 6, INV>(a[11]);
+    a[13] = wconst_mul<T, 16, 3, INV>(a[13]);
+    a[14] = wconst_mul<T, 16, 6, INV>(a[14]);
+    a[15] = wconst_mul<T, 16, 9, INV>(a[15]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4<T, INV>(a[4 * k1], a[4 * k1 + 1], a[4 * k1 + 2], a[4 * k1 + 3]);
+    // a[4 k1 + k2] holds X[k1 + 4 k2]: transpose the 4x4 index map into natural order
+    C<T> t[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) t[k1 + 4 * k2] = a[4 * k1 + k2];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = t[k];
+  } else {
+    static_assert(R <= 16, "radix > 16");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// IEEE bit flip (reference fault.py:25-38) on one component of a complex value
+
+__device__ __forceinline__ float flip_bits(float v, int bit) {
+  return __uint_as_float(__float_as_uint(v) ^ (1u << bit));
+}
+__device__ __forceinline__ double flip_bits(double v, int bit) {
+  return __longlong_as_double(__double_as_longlong(v) ^ (1ll << bit));
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk async copy (TMA 1-D) helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TFFT_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TFFT_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// streaming (evict-first) global store of one complex value
+__device__ __forceinline__ void st_cs(float2* p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_cs(double2* p, double2 v) { __stcs(p, v); }
+
+template <typename T> __device__ __forceinline__ bool finite2(C<T> v) { return isfinite(v.x) && isfinite(v.y); }
+
+// XOR swizzle (element units) so Stockham scatter writes hit distinct banks:
+// 16 float2 / 8 double2 slots per 128-byte bank row.
+template <typename T> __device__ __forceinline__ int swz(int a) {
+  if constexpr (sizeof(T) == 4) return a ^ ((a >> 4) & 15);
+  else return a ^ ((a >> 3) & 7);
+}
+
+}  // namespace tfft

@@ -1,0 +1,497 @@
+// K1 / K2: single-pass batched FFT (N <= 2^13 FP32, 2^12 FP64), optionally with
+// the fused two-sided ABFT epilogue (reference abft.py:592-665 done on-chip).
+//
+// Persistent CTAs; each CTA owns SPT "slots" of TPS threads, one signal per slot
+// per pipeline step. Signal tiles arrive through 1-D bulk async copies
+// (cp.async.bulk, the TMA engine) into an NSTAGE-deep shared-memory ring
+// guarded by mbarriers, so HBM reads for step i+NSTAGE-1 overlap the radix work
+// of step i. The FFT runs in place in the stage buffer; the last pass stores
+// straight from registers to HBM (coalesced: thread tau writes tau + TPS*k).
+//
+// ABFT (template flag, zero cost when off): per signal, c_in = row . x and the
+// floor ||x||^2 are formed from the registers the first pass loaded, c_out =
+// enc . y from the registers the last pass stores; per verification window,
+// s_in = sum w_j x_j and s_out = sum w_j y_j accumulate in registers across the
+// window's signals and FFT(s_in) runs in-CTA at the window end. No extra HBM
+// traffic beyond O(B) scalars and O(#windows) partial columns.
+#include "tfft_fft.cuh"
+#include "tfft_internal.h"
+
+namespace tfft {
+
+template <typename T, int LOGN, bool INV, bool ABFT>
+struct K1 {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int EMAX = sizeof(T) == 4 ? 16 : 8;
+  using F = Fft<T, N, EMAX, INV>;
+  static constexpr int E = F::E;
+  static constexpr int TPS = F::TPS;
+  static constexpr int NT_TARGET = 256;
+  static constexpr int SPT = TPS >= NT_TARGET ? 1 : NT_TARGET / TPS;
+  static constexpr int NT = SPT * TPS;
+  static constexpr int TILE = SPT * N;
+  static constexpr int TILE_BYTES = TILE * (int)sizeof(C<T>);
+  static constexpr int NSTAGE = TILE_BYTES <= 32768 ? 3 : 2;
+  static constexpr int NWARP_SLOT = TPS >= 32 ? TPS / 32 : 1;
+  static constexpr int RED_BYTES = SPT * NWARP_SLOT * 5 * 8;
+  static constexpr int SMEM = (NSTAGE + (ABFT ? 1 : 0)) * TILE_BYTES + RED_BYTES + 64 + NSTAGE * 8;
+};
+
+// deterministic reduction of NV doubles over the TPS threads of a slot;
+// result valid in the slot's tau == 0 thread. Contains a CTA barrier when
+// TPS > 32 (every thread must call).
+template <int TPS, int NV>
+__device__ __forceinline__ void slot_reduce(double (&r)[NV], double* red, int g, int tau) {
+  if constexpr (TPS <= 32) {
+#pragma unroll
+    for (int off = TPS / 2; off >= 1; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) r[k] += __shfl_xor_sync(0xffffffffu, r[k], off);
+  } else {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) r[k] += __shfl_xor_sync(0xffffffffu, r[k], off);
+    constexpr int NW = TPS / 32;
+    const int w = tau >> 5;
+    if ((tau & 31) == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) red[(g * NW + w) * NV + k] = r[k];
+    __syncthreads();
+    if (tau == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        double acc = red[(g * NW) * NV + k];
+        for (int i = 1; i < NW; ++i) acc += red[(g * NW + i) * NV + k];
+        r[k] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* addr, double v) {
+  atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+template <typename T, int LOGN, bool INV, bool ABFT>
+__global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a) {
+  using K = K1<T, LOGN, INV, ABFT>;
+  using F = typename K::F;
+  using CT = C<T>;
+  constexpr int N = K::N, E = K::E, TPS = K::TPS, SPT = K::SPT, NSTAGE = K::NSTAGE;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  CT* tiles = reinterpret_cast<CT*>(smem);
+  CT* wbuf = tiles + NSTAGE * K::TILE;  // ABFT window buffer (one tile)
+  double* red = reinterpret_cast<double*>(smem + (NSTAGE + (ABFT ? 1 : 0)) * K::TILE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(red) + K::RED_BYTES);
+  int* flag = reinterpret_cast<int*>(full + NSTAGE);
+
+  const int tid = threadIdx.x;
+  const int g = tid / TPS;
+  const int tau = tid % TPS;
+  const CT* __restrict__ x = static_cast<const CT*>(a.x);
+  CT* __restrict__ y = static_cast<CT*>(a.y);
+  const CT* __restrict__ tw = static_cast<const CT*>(a.tw);
+  const int64_t B = a.batch;
+
+  // ---- work decomposition --------------------------------------------------
+  // plain: item k = tile of SPT consecutive signals (one step)
+  // ABFT mode 0: item k = SPT consecutive windows, slot g runs window k*SPT+g
+  // ABFT mode 1: item k = piece (k % P) of window (k / P), split over the slots
+  const int64_t W = ABFT ? a.abft.win_signals : 1;
+  const int64_t P = ABFT ? a.abft.pieces : 1;
+  const int mode = ABFT ? a.abft.mode : 0;
+  int64_t nitems;
+  if (!ABFT) nitems = (B + SPT - 1) / SPT;
+  else if (mode == 0) nitems = (a.abft.nwin + SPT - 1) / SPT;
+  else nitems = a.abft.nwin * P;
+
+  auto slot_run = [&](int64_t item, int gg, int64_t& start, int64_t& len) {
+    if (!ABFT) {
+      start = item * SPT + gg;
+      len = start < B ? 1 : 0;
+    } else if (mode == 0) {
+      const int64_t w = item * SPT + gg;
+      start = w * W;
+      len = (w < a.abft.nwin) ? min(W, B - start) : 0;
+    } else {
+      const int64_t wi = item / P, pi = item % P;
+      const int64_t w0 = wi * W, w1 = min(w0 + W, B);
+      const int64_t pl = (W + P - 1) / P;
+      const int64_t ps = min(w0 + pi * pl, w1), pe = min(ps + pl, w1);
+      const int64_t sl = (pe - ps + SPT - 1) / SPT;
+      start = min(ps + gg * sl, pe);
+      len = min(start + sl, pe) - start;
+    }
+    if (len < 0) len = 0;
+  };
+  auto item_len = [&](int64_t item) {
+    int64_t s, l, mx = 0;
+    for (int gg = 0; gg < SPT; ++gg) {
+      slot_run(item, gg, s, l);
+      mx = l > mx ? l : mx;
+    }
+    return mx;
+  };
+
+  // ---- producer (thread 0): issues the bulk copies of one pipeline step ------
+  int64_t p_item = blockIdx.x, p_i = 0, p_len = 0;
+  if (tid == 0) {
+#pragma unroll 1
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    p_len = p_item < nitems ? item_len(p_item) : 0;
+  }
+  __syncthreads();
+  auto produce = [&](int stage) {  // thread 0 only
+    while (p_item < nitems && p_i >= p_len) {
+      p_item += gridDim.x;
+      p_i = 0;
+      p_len = p_item < nitems ? item_len(p_item) : 0;
+    }
+    if (p_item >= nitems) return;
+    CT* dst = tiles + stage * K::TILE;
+    if (!ABFT) {
+      const int64_t s0 = p_item * SPT;
+      const int64_t cnt = min((int64_t)SPT, B - s0);
+      const uint32_t bytes = (uint32_t)(cnt * N * sizeof(CT));
+      mbar_expect_tx(&full[stage], bytes);
+      bulk_g2s(dst, x + s0 * N, bytes, &full[stage]);
+    } else {
+      uint32_t bytes = 0;
+      int64_t st[SPT];
+      bool ok[SPT];
+      for (int gg = 0; gg < SPT; ++gg) {
+        int64_t s, l;
+        slot_run(p_item, gg, s, l);
+        ok[gg] = p_i < l;
+        st[gg] = s + p_i;
+        bytes += ok[gg] ? (uint32_t)(N * sizeof(CT)) : 0u;
+      }
+      mbar_expect_tx(&full[stage], bytes);
+      for (int gg = 0; gg < SPT; ++gg)
+        if (ok[gg]) bulk_g2s(dst + gg * N, x + st[gg] * N, N * sizeof(CT), &full[stage]);
+    }
+    ++p_i;
+  };
+  if (tid == 0)
+    for (int s = 0; s < NSTAGE; ++s) produce(s);
+
+  // ---- ABFT per-thread state -------------------------------------------------
+  CT s_in[ABFT ? E : 1], s_out[ABFT ? E : 1];
+  int enc_mod3[ABFT ? E : 1];
+  if constexpr (ABFT) {
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      s_in[k] = mk<T>(0, 0);
+      s_out[k] = mk<T>(0, 0);
+      enc_mod3[k] = (tau + TPS * F::out_pos(k)) % 3;
+    }
+  }
+  const CT* __restrict__ row = static_cast<const CT*>(a.abft.row);
+  bool bad_input = false;
+
+  uint32_t it = 0;
+#pragma unroll 1
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    int64_t my_start, my_len;
+    slot_run(item, g, my_start, my_len);
+    const int64_t len = item_len(item);
+#pragma unroll 1
+    for (int64_t i = 0; i < len; ++i, ++it) {
+      const int stage = it % NSTAGE;
+      mbar_wait(&full[stage], (it / NSTAGE) & 1);
+      CT* buf = tiles + stage * K::TILE + g * N;
+      const bool valid = i < my_len;
+      const int64_t sig = my_start + i;
+
+      CT v[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = buf[tau + TPS * k];
+      if (valid) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) bad_input |= !finite2<T>(v[k]);
+      }
+
+      double red5[5] = {0, 0, 0, 0, 0};
+      if constexpr (ABFT) {
+        if (valid) {
+          // c_in = row . x and ||x||^2 from the clean input (abft.py:656-659)
+          CT ci = mk<T>(0, 0);
+          T fl = 0;
+          const T w = (T)(a.weight0 + sig + 1);
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const CT r = __ldg(row + tau + TPS * k);
+            ci = cadd<T>(ci, cmul<T>(r, v[k]));
+            fl = rfma(v[k].x, v[k].x, rfma(v[k].y, v[k].y, fl));
+            s_in[k] = mk<T>(rfma(w, v[k].x, s_in[k].x), rfma(w, v[k].y, s_in[k].y));
+          }
+          red5[0] = (double)ci.x;
+          red5[1] = (double)ci.y;
+          red5[2] = (double)fl;
+        }
+      }
+      // stage-0 strikes: flip the freshly loaded element (fault.py:99-107)
+      if (a.nfaults > 0 && valid) {
+        for (int f = 0; f < a.nfaults; ++f) {
+          const DevFault fl = a.faults[f];
+          if (fl.signal != sig || fl.stage != 0 || (int)(fl.element % TPS) != tau) continue;
+          const int k0 = (int)(fl.element / TPS);
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (k == k0) {
+              if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
+              else v[k].y = flip_bits(v[k].y, fl.bit);
+            }
+        }
+      }
+
+      F::run(buf, v, tau, tw);
+      fence_proxy_async();
+      __syncthreads();  // every read of this stage buffer is done: refill it
+      if (tid == 0) produce(stage);
+
+      if constexpr (INV) {
+        const T sc = (T)(1.0 / (double)N);
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = cscale<T>(v[k], sc);
+      }
+      if (valid) {
+        CT* yo = y + sig * N + tau;
+#pragma unroll
+        for (int k = 0; k < E; ++k) st_cs(yo + TPS * F::out_pos(k), v[k]);
+      }
+      if constexpr (ABFT) {
+        if (valid) {
+          const T w = (T)(a.weight0 + sig + 1);
+          CT co = mk<T>(0, 0);
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const int pk = F::out_pos(k);
+            CT e;
+            if (a.abft.enc == ENC_WANG) {
+              const T h = (T)0.86602540378443864676372317075294;  // sin(2 pi/3)
+              const int m = enc_mod3[k];
+              e = m == 0 ? mk<T>(1, 0) : (m == 1 ? mk<T>((T)-0.5, -h) : mk<T>((T)-0.5, h));
+            } else if (a.abft.enc == ENC_ONES) {
+              e = mk<T>(1, 0);
+            } else {
+              e = __ldg(tw + tau + TPS * pk);  // omega_N^k (forward table)
+            }
+            co = cadd<T>(co, cmul<T>(e, v[k]));
+            s_out[pk] = mk<T>(rfma(w, v[k].x, s_out[pk].x), rfma(w, v[k].y, s_out[pk].y));
+          }
+          red5[3] = (double)co.x;
+          red5[4] = (double)co.y;
+        }
+        slot_reduce<TPS, 5>(red5, red, g, tau);
+        if (valid && tau == 0) {
+          const double cin_r = red5[0], cin_i = red5[1];
+          const double co_r = red5[3], co_i = red5[4];
+          const double floor_v = sqrt(red5[2]) / sqrt((double)N);
+          double dv;
+          if (!isfinite(co_r) || !isfinite(co_i)) {
+            dv = __longlong_as_double(0x7ff0000000000000ll);
+          } else {
+            const double den = fmax(fmax(hypot(cin_r, cin_i), floor_v), 1e-30);
+            dv = hypot(cin_r - co_r, cin_i - co_i) / den;
+          }
+          a.abft.c_in[2 * sig] = cin_r;
+          a.abft.c_in[2 * sig + 1] = cin_i;
+          a.abft.c_out[2 * sig] = co_r;
+          a.abft.c_out[2 * sig + 1] = co_i;
+          a.abft.floors[sig] = floor_v;
+          a.abft.div[sig] = dv;
+          if (dv > a.abft.delta) atomicAdd(&a.counters->triggered, 1ull);
+          atomic_max_nonneg(&a.counters->max_div_bits, dv);
+        }
+      }
+    }
+
+    // ---- end of item: verification-window work (abft.py:592-624, fused) -----
+    if constexpr (ABFT) {
+      const int64_t wi_mode1 = item / P;
+      bool have_window = false;  // this slot (mode 0) / slot 0 (mode 1) finalizes a window
+      int64_t wid = 0;
+      if (mode == 0) {
+        wid = item * SPT + g;
+        have_window = wid < a.abft.nwin;
+        if (have_window) {
+#pragma unroll
+          for (int k = 0; k < E; ++k) wbuf[g * N + tau + TPS * k] = s_in[k];
+        }
+        __syncthreads();
+      } else {
+        // combine the slots' partials in slot order, then (if the window is split
+        // into pieces) publish the piece partial; the last piece finalizes
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+          for (int k = 0; k < E; ++k) wbuf[g * N + tau + TPS * k] = pass == 0 ? s_in[k] : s_out[k];
+          __syncthreads();
+          if (g == 0) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+              CT acc = wbuf[tau + TPS * k];
+              for (int gg = 1; gg < SPT; ++gg) acc = cadd<T>(acc, wbuf[gg * N + tau + TPS * k]);
+              if (pass == 0) s_in[k] = acc;
+              else s_out[k] = acc;
+            }
+          }
+          __syncthreads();
+        }
+        wid = wi_mode1;
+        bool last = true;
+        if (P > 1) {
+          CT* ws = static_cast<CT*>(a.abft.ws) + item * 2 * N;
+          if (g == 0) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+              ws[tau + TPS * k] = s_in[k];
+              ws[N + tau + TPS * k] = s_out[k];
+            }
+          }
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) {
+            const unsigned prev = atomicAdd(&a.abft.win_count[wid], 1u);
+            *flag = (prev == (unsigned)(P - 1));
+          }
+          __syncthreads();
+          last = *flag != 0;
+          if (last) {
+            __threadfence();
+            if (g == 0) {
+              const CT* wsw = static_cast<const CT*>(a.abft.ws) + wid * P * 2 * N;
+#pragma unroll
+              for (int k = 0; k < E; ++k) {
+                CT ai = __ldcg(wsw + tau + TPS * k);
+                CT ao = __ldcg(wsw + N + tau + TPS * k);
+                for (int64_t pi = 1; pi < P; ++pi) {
+                  ai = cadd<T>(ai, __ldcg(wsw + pi * 2 * N + tau + TPS * k));
+                  ao = cadd<T>(ao, __ldcg(wsw + pi * 2 * N + N + tau + TPS * k));
+                }
+                s_in[k] = ai;
+                s_out[k] = ao;
+              }
+            }
+            if (tid == 0) a.abft.win_count[wid] = 0;
+          }
+        }
+        have_window = last && g == 0;
+        if (last) {
+          if (g == 0) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) wbuf[tau + TPS * k] = s_in[k];
+          }
+          __syncthreads();
+        }
+        if (!last) {
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            s_in[k] = mk<T>(0, 0);
+            s_out[k] = mk<T>(0, 0);
+          }
+          continue;
+        }
+      }
+      // in-CTA FFT of s_in (working precision, as _fft_column) vs s_out
+      CT v[E];
+      CT* wb = wbuf + g * N;
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = wb[tau + TPS * k];
+      F::run(wb, v, tau, tw);
+      double r2[2] = {0, 0};
+      if (have_window) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const int pk = F::out_pos(k);
+          const double dr = (double)v[k].x - (double)s_out[pk].x;
+          const double di = (double)v[k].y - (double)s_out[pk].y;
+          r2[0] += dr * dr + di * di;
+          r2[1] += (double)v[k].x * (double)v[k].x + (double)v[k].y * (double)v[k].y;
+        }
+      }
+      slot_reduce<TPS, 2>(r2, red, g, tau);
+      if (have_window && tau == 0) a.abft.win_div[wid] = sqrt(r2[0]) / fmax(sqrt(r2[1]), 1e-30);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        s_in[k] = mk<T>(0, 0);
+        s_out[k] = mk<T>(0, 0);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad_input) && (tid & 31) == 0) atomicOr(&a.counters->nonfinite, 1ull);
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+
+template <typename T, int LOGN, bool INV, bool ABFT>
+static int launch_one(const K1Args& a, int num_sms, cudaStream_t st) {
+  using K = K1<T, LOGN, INV, ABFT>;
+  auto kern = k1_kernel<T, LOGN, INV, ABFT>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM);
+  if (e != cudaSuccess) return (int)e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t nitems;
+  if (!ABFT) nitems = (a.batch + K::SPT - 1) / K::SPT;
+  else if (a.abft.mode == 0) nitems = (a.abft.nwin + K::SPT - 1) / K::SPT;
+  else nitems = a.abft.nwin * a.abft.pieces;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > nitems) grid = nitems;
+  if (grid < 1) return 0;
+  kern<<<(unsigned)grid, K::NT, K::SMEM, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, bool INV, bool ABFT>
+static int dispatch(int logn, const K1Args& a, int num_sms, cudaStream_t st) {
+  switch (logn) {
+#define TFFT_CASE(L) \
+  case L: return launch_one<T, L, INV, ABFT>(a, num_sms, st);
+    TFFT_CASE(1) TFFT_CASE(2) TFFT_CASE(3) TFFT_CASE(4) TFFT_CASE(5) TFFT_CASE(6) TFFT_CASE(7)
+    TFFT_CASE(8) TFFT_CASE(9) TFFT_CASE(10) TFFT_CASE(11) TFFT_CASE(12)
+#undef TFFT_CASE
+    case 13:
+      if constexpr (sizeof(T) == 4) return launch_one<T, 13, INV, ABFT>(a, num_sms, st);
+      return (int)cudaErrorInvalidValue;
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
+int k1_supported(int prec, int logn) { return logn >= 1 && logn <= (prec == 0 ? 13 : 12); }
+
+int launch_k1(int prec, int logn, bool inverse, bool abft, const K1Args& a, int num_sms, cudaStream_t st) {
+  if (!k1_supported(prec, logn)) return (int)cudaErrorInvalidValue;
+  if (prec == 0) {
+    if (abft) return dispatch<float, false, true>(logn, a, num_sms, st);
+    return inverse ? dispatch<float, true, false>(logn, a, num_sms, st) : dispatch<float, false, false>(logn, a, num_sms, st);
+  }
+  if (abft) return dispatch<double, false, true>(logn, a, num_sms, st);
+  return inverse ? dispatch<double, true, false>(logn, a, num_sms, st) : dispatch<double, false, false>(logn, a, num_sms, st);
+}
+
+}  // namespace tfft
+
+namespace tfft {
+int k1_slots(int prec, int logn) {
+  const int n = 1 << logn;
+  const int emax = prec == 0 ? 16 : 8;
+  const int e = emax < n ? emax : n;
+  const int tps = n / e;
+  return tps >= 256 ? 1 : 256 / tps;
+}
+}  // namespace tfft

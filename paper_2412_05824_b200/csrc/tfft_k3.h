@@ -1,0 +1,29 @@
+// K3 / K4: two-pass (four-step) batched FFT for N beyond the single-pass range,
+// optionally with the fused ABFT epilogue. Library-private.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tfft_internal.h"
+
+namespace tfft {
+
+struct K3Plan;
+
+int k3_create(int64_t n, int prec, const int64_t* spans, int nstages, int num_sms, K3Plan** out);
+void k3_destroy(K3Plan* p);
+int k3_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults, int nfaults,
+               Counters* counters, void* reserved, cudaStream_t st);
+int k3_protected(K3Plan* p, const void* x, void* y, int64_t batch, int64_t weight0, const DevFault* faults,
+                 int nfaults, Counters* counters, const AbftArgs& ab, const void* row, cudaStream_t st);
+// omega_(s r)^q for q < s into dst (working precision, conj for inverse)
+int k3_base_table(K3Plan* p, int prec, int64_t s, int r, int inverse, void* dst, cudaStream_t st);
+// true when the two-pass split equals the reference's first stage span, so
+// stage-1 strikes land in-kernel on the canonical intermediate
+bool k3_strikes_stage1(const K3Plan* p);
+// omega_N^k / conj tables (built lazily; only the Jou encoding reads them)
+const void* k3_enc_table(K3Plan* p);
+const void* k3_enc_table_inv(K3Plan* p);
+
+}  // namespace tfft

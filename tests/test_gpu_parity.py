@@ -1,0 +1,189 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference's golden
+fixtures and the pinned CPU oracle, on the same seeded inputs."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import (EPS, gaussian, golden, golden_abft_outputs, golden_fft_outputs, l2_tol, max_rel_error,
+                      oracle_tol, rel_l2)
+
+pytestmark = pytest.mark.gpu
+
+
+def _tf():
+    import paper_2412_05824_b200 as tf
+    return tf
+
+
+def plan_of(case):
+    tf = _tf()
+    return tf.build_plan(tf.PlanParams(tuple(case["spans"]), tuple(case["radices"]), case["bs"]), case["precision"])
+
+
+def arm(plan, batch, specs, seu=False):
+    tf = _tf()
+    inj = tf.FaultInjector(seu=seu)
+    for s in specs:
+        inj.arm(tf.FaultSpec(**s), plan=plan, batch=batch)
+    return inj
+
+
+@pytest.mark.parametrize("case", golden()["fft_cases"], ids=lambda c: c["name"])
+def test_transform_matches_reference(case):
+    tf = _tf()
+    x = gaussian(case["n"], case["b"], case["precision"], case["seed"])
+    plan = plan_of(case)
+    batch = tf.SignalBatch(x)
+    inj = arm(plan, batch, case["faults"]) if case["faults"] else None
+    y = tf.execute_plan(plan, batch, case["direction"], injector=inj).data
+    ref = golden_fft_outputs()[case["name"]]
+    if not case["faults"]:
+        assert rel_l2(y, ref) <= l2_tol(case["precision"], case["n"])
+        assert max_rel_error(y, ref) <= oracle_tol(case["precision"], case["n"])
+    else:
+        # a flipped exponent can make the faulted signal's bins huge; compare
+        # per signal against its own scale, and the untouched rows bitwise-close
+        for r in range(case["b"]):
+            scale = max(np.abs(ref[r]).max(), 1e-300)
+            err = np.abs(y[r] - ref[r]).max() / scale
+            assert err <= 4 * oracle_tol(case["precision"], case["n"]), (r, err)
+
+
+@pytest.mark.parametrize("case", golden()["abft_cases"], ids=lambda c: c["name"])
+def test_protected_decisions_match_reference(case):
+    tf = _tf()
+    x = gaussian(case["n"], case["b"], case["precision"], case["seed"])
+    plan = plan_of(case)
+    batch = tf.SignalBatch(x)
+    kw = dict(case["kwargs"])
+    faults = kw.pop("faults", [])
+    seu = kw.pop("seu", True)
+    offline = kw.pop("offline", False)
+    kind = kw.pop("kind", "wang")
+    inj = arm(plan, batch, faults, seu=seu) if faults else None
+    stats = tf.RunStats()
+    if offline:
+        out, reports = tf.run_offline(plan, batch, e_left=kind, injector=inj, stats=stats)
+    else:
+        out, reports = tf.run_protected(plan, batch, e_left=kind, group_size=kw.get("T", 1),
+                                        mode=kw.get("mode", "fused"), injector=inj, stats=stats)
+    r = case["result"]
+    assert [(e.transaction, e.signal) for e in stats.events] == [(e[0], e[1]) for e in r["events"]]
+    for e in stats.events:
+        assert e.located in (None, e.signal)
+    assert (stats.signal_sweeps, stats.verifications, stats.corrections, stats.recomputations) == (
+        r["signal_sweeps"], r["verifications"], r["corrections"], r["recomputations"])
+    assert [(x_.triggered, x_.corrected, x_.uncorrectable, x_.verification_index) for x_ in reports] == [
+        (q[0], q[1], q[2], q[4]) for q in r["reports"]]
+    ref = golden_abft_outputs()[case["name"]]
+    assert max_rel_error(out.data, ref) <= 2 * oracle_tol(case["precision"], case["n"])
+
+
+@pytest.mark.parametrize("camp", golden()["campaigns"], ids=lambda c: c["name"])
+def test_campaign_fault_locations_bit_exact(camp):
+    """north_star: the set of detected and corrected fault locations is bit-exact."""
+    tf = _tf()
+    from paper_2412_05824_b200 import fault as F
+    plan = tf.build_plan(tf.select_params(camp["n"], camp["b"], camp["precision"]), camp["precision"])
+    mismatches = []
+    for trial, rec in enumerate(camp["trials"]):
+        rng = np.random.default_rng((camp["seed"], trial))
+        batch = F._gaussian_batch(rng, camp["n"], camp["b"], camp["precision"])
+        spec = F._draw_spec(rng, plan, batch)
+        assert dict(transaction=spec.transaction, signal=spec.signal, element=spec.element, stage=spec.stage,
+                    part=spec.part, bit=spec.bit) == rec["spec"]
+        inj = tf.FaultInjector()
+        inj.arm(spec, plan=plan, batch=batch)
+        stats = tf.RunStats()
+        _, reports = tf.run_protected(plan, batch, group_size=camp["T"], injector=inj, stats=stats)
+        got = ([(e.transaction, e.signal) for e in stats.events], stats.corrections, stats.recomputations,
+               [(q.triggered, q.corrected, q.uncorrectable) for q in reports])
+        want = ([(e[0], e[1]) for e in rec["events"]], rec["corrections"], rec["recomputations"],
+                [tuple(q[:3]) for q in rec["reports"]])
+        if got != want:
+            mismatches.append((trial, got, want, rec["max_divergence"], stats.max_divergence))
+    assert not mismatches, mismatches[:3]
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192])
+def test_oracle_equivalence_and_bitwise_protected(precision, n):
+    """Reference test_fft_core.py:115-123 + test_abft.py:197-206 on the GPU."""
+    tf = _tf()
+    from oracle import ref_oracle as O
+    b = 37
+    x = gaussian(n, b, precision, seed=n + 5)
+    params = tf.select_params(n, b, precision)
+    plan = tf.build_plan(params, precision)
+    y = tf.execute_plan(plan, tf.SignalBatch(x)).data
+    ref = O.execute(x, O.select_params(n, b, precision))
+    assert rel_l2(y, ref) <= l2_tol(precision, n)
+    assert max_rel_error(y, ref) <= oracle_tol(precision, n)
+    for T in (1, 3):
+        stats = tf.RunStats()
+        out, reports = tf.run_protected(plan, tf.SignalBatch(x), group_size=T, stats=stats)
+        assert np.array_equal(out.data, y)
+        assert not any(r.triggered for r in reports)
+        ntx = -(-b // params.bs)
+        assert len(reports) == -(-ntx // T)
+        assert stats.max_divergence <= tf.default_delta(precision)
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+@pytest.mark.parametrize("n", [256, 1024, 4096])
+def test_roundtrip(precision, n):
+    tf = _tf()
+    x = gaussian(n, 5, precision, seed=3)
+    plan = tf.build_plan(tf.select_params(n, 5, precision), precision)
+    back = tf.execute_plan(plan, tf.execute_plan(plan, tf.SignalBatch(x)), "inverse").data
+    assert max_rel_error(back, x) <= (1e-5 if precision == "single" else 1e-12)
+
+
+def test_nonfinite_input_rejected():
+    tf = _tf()
+    x = gaussian(256, 3, "single", seed=1)
+    x[1, 7] = np.inf
+    plan = tf.build_plan(tf.select_params(256, 3, "single"), "single")
+    with pytest.raises(ValueError):
+        tf.execute_plan(plan, tf.SignalBatch(x))
+    with pytest.raises(ValueError):
+        tf.run_protected(plan, tf.SignalBatch(x))
+
+
+def test_device_resident_batch_stays_on_device():
+    tf = _tf()
+    import torch
+    x = gaussian(1024, 8, "single", seed=2)
+    plan = tf.build_plan(tf.select_params(1024, 8, "single"), "single")
+    xd = torch.from_numpy(x).cuda()
+    y = tf.execute_plan(plan, tf.SignalBatch(xd))
+    assert y.on_device
+    assert np.array_equal(y.data.cpu().numpy(), tf.execute_plan(plan, tf.SignalBatch(x)).data)
+
+
+def test_stockham_pass_boundary_and_butterflies():
+    """The plugin kernel itself (_kernels.pyx:74-84) vs the reference's pass."""
+    tf = _tf()
+    from oracle import ref_oracle as O
+    from paper_2412_05824_b200 import backend
+    rng = np.random.default_rng(5)
+    for dt in (np.complex64, np.complex128):
+        for (n, s, r) in [(64, 1, 4), (64, 4, 4), (64, 16, 2), (128, 8, 4), (32, 16, 2)]:
+            src = (rng.standard_normal((3, n)) + 1j * rng.standard_normal((3, n))).astype(dt)
+            base = O.base_table(s, r, dt)
+            for inv in (False, True):
+                b = np.conj(base) if inv else base
+                got = np.empty_like(src)
+                backend.kernel().stockham_pass(src, got, s, r, b, inv)
+                want = np.empty_like(src)
+                O.stockham_pass_np(src, want, s, r, b, inv)
+                assert np.abs(got - want).max() <= 8 * np.finfo(dt).eps * np.abs(want).max()
+        with pytest.raises(ValueError):
+            backend.kernel().stockham_pass(src, np.empty_like(src), 1, 8, O.base_table(1, 8, dt), False)
+    for r in (2, 4, 8, 16, 32):
+        u = rng.standard_normal(r) + 1j * rng.standard_normal(r)
+        got = tf.butterfly_radix(u, r)
+        ref = np.fft.fft(u)
+        assert np.abs(got - ref).max() <= 8 * EPS["double"] * np.abs(ref).max()
