@@ -119,7 +119,10 @@ struct tfft_plan {
   int num_sms = 148;
   int device = 0;
   bool k1 = false;
+  int mode = 0;              // 0: K1 single pass, 1: K3 two pass, 2: reference-order multipass
   DevBuf tw_fwd, tw_inv;     // omega_N^k, conj (K1 and ABFT encodings)
+  DevBuf enc_tab[2];         // omega_N^k / conj for K3/multipass Jou encoding (lazy)
+  DevBuf wsum;               // unfused window sums (s_in, s_out, FFT(s_in))
   DevBuf rows[3];            // left checksum rows per encoding kind
   bool row_ready[3] = {false, false, false};
   DevBuf counters;           // default counters
@@ -218,7 +221,7 @@ int strike_path(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse
           base = tw.p;
           stride = p->n / (ps.s * ps.r);
         } else {
-          TFFT_TRY(k3_base_table(p->k3, p->prec, ps.s, ps.r, inverse, p->base.p, st), "strike base table");
+          TFFT_TRY(launch_base_table(p->prec, ps.s, ps.r, inverse, p->base.p, st), "strike base table");
           base = p->base.p;
           stride = 1;
         }
@@ -258,7 +261,7 @@ int split_faults(tfft_plan* p, const tfft_fault* faults, int nfaults, int64_t si
     if (f.element < 0 || f.element >= p->n || f.stage < 0 || f.stage >= (int)p->spans.size() || f.bit < 0 ||
         f.bit >= (p->prec == 0 ? 32 : 64) || (f.part != 0 && f.part != 1))
       return fail(TFFT_EINVAL, "fault spec out of range");
-    const bool in_kernel = f.stage == 0 || (k3_split_ok && f.stage == 1 && !p->k1 && k3_strikes_stage1(p->k3));
+    const bool in_kernel = p->mode != 2 && (f.stage == 0 || (k3_split_ok && f.stage == 1 && p->mode == 1 && k3_strikes_stage1(p->k3)));
     if (in_kernel) dev.push_back({r, f.element, f.stage, f.part, f.bit, 0});
     else slow.push_back(f);
   }
@@ -272,6 +275,39 @@ int upload_faults(tfft_plan* p, const std::vector<DevFault>& dev, cudaStream_t s
   TFFT_TRY((int)cudaMemcpyAsync(p->faults.p, dev.data(), dev.size() * sizeof(DevFault), cudaMemcpyHostToDevice, st),
            "fault upload");
   return 0;
+}
+
+// sizes beyond the fused kernels: the reference's own radix-4/2 pass list, one
+// device sweep per pass (correct for any N up to 2^29; not the fast path)
+int multipass(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, cudaStream_t st) {
+  const size_t cb = cbytes(p->prec);
+  int e = p->scratch_b.ensure((size_t)batch * p->n * cb);
+  if (!e) e = p->base.ensure((size_t)p->n * cb);
+  if (e) return cuda_fail(e, "multipass scratch");
+  const size_t np = p->passes.size();
+  void* bufs[2] = {y, p->scratch_b.p};
+  const void* cur = x;
+  for (size_t i = 0; i < np; ++i) {
+    const auto& ps = p->passes[i];
+    void* out = bufs[(np - 1 - i) % 2];
+    TFFT_TRY(launch_base_table(p->prec, ps.s, ps.r, inverse, p->base.p, st), "multipass base table");
+    TFFT_TRY(launch_stockham_pass(p->prec, cur, out, batch, p->n, ps.s, ps.r, p->base.p, 1, inverse, st),
+             "multipass pass");
+    cur = out;
+  }
+  if (inverse) TFFT_TRY(launch_scale(p->prec, y, batch * p->n, 1.0 / (double)p->n, st), "multipass scale");
+  return 0;
+}
+
+const void* enc_table(tfft_plan* p, bool inv) {
+  if (p->k1) return inv ? p->tw_inv.p : p->tw_fwd.p;
+  DevBuf& b = p->enc_tab[inv ? 1 : 0];
+  if (!b.p) {
+    if (b.ensure((size_t)p->n * cbytes(p->prec))) return nullptr;
+    launch_base_table(p->prec, p->n, 1, inv ? 1 : 0, b.p, 0);
+    cudaDeviceSynchronize();
+  }
+  return b.p;
 }
 
 int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, int64_t signal_offset,
@@ -289,10 +325,13 @@ int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, 
     TFFT_TRY(launch_k1(p->prec, p->logn, inverse != 0, false, a, p->num_sms, st), "k1 launch");
     return 0;
   }
-  int rc = k3_execute(p->k3, x, y, batch, inverse, (const DevFault*)p->faults.p, (int)dev.size(), (Counters*)counters,
-                      nullptr, st);
-  g_launches.fetch_add(2, std::memory_order_relaxed);
-  return rc ? cuda_fail(rc, "k3 launch") : 0;
+  if (p->mode == 1) {
+    int rc = k3_execute(p->k3, x, y, batch, inverse, (const DevFault*)p->faults.p, (int)dev.size(),
+                        (Counters*)counters, nullptr, st);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return rc ? cuda_fail(rc, "k3 launch") : 0;
+  }
+  return multipass(p, x, y, batch, inverse, st);
 }
 
 }  // namespace
@@ -352,11 +391,14 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
     }
   } else {
     int rc = k3_create(n, precision, p->spans.data(), (int)p->spans.size(), p->num_sms, &p->k3);
-    if (rc) {
-      std::string msg = g_err.empty() ? std::string("k3 plan") : g_err;
+    if (rc == (int)cudaErrorInvalidValue) {
+      p->mode = 2;
+      p->k3 = nullptr;
+    } else if (rc) {
       tfft_plan_destroy(p);
-      return rc == (int)cudaErrorInvalidValue ? fail(TFFT_EUNSUPPORTED, "unsupported size for the two-pass kernel")
-                                              : cuda_fail(rc, "k3 plan");
+      return cuda_fail(rc, "k3 plan");
+    } else {
+      p->mode = 1;
     }
   }
   *out = p;
@@ -365,7 +407,7 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
 
 int tfft_plan_destroy(tfft_plan* p) {
   if (!p) return TFFT_OK;
-  DevBuf* all[] = {&p->tw_fwd, &p->tw_inv, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
+  DevBuf* all[] = {&p->tw_fwd, &p->tw_inv, &p->enc_tab[0], &p->enc_tab[1], &p->wsum, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
                    &p->ws, &p->win_count, &p->scratch_a, &p->scratch_b, &p->base, &p->col_a, &p->col_b, &p->col64};
   for (DevBuf* b : all) b->release();
   if (p->k3) k3_destroy(p->k3);
@@ -457,10 +499,32 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     a.abft = ab;
     TFFT_TRY(launch_k1(p->prec, p->logn, false, true, a, p->num_sms, st), "k1 abft launch");
   } else {
-    int e = k3_protected(p->k3, x, y, batch, signal_offset, (const DevFault*)p->faults.p, (int)dev.size(),
-                         (Counters*)counters, ab, p->rows[enc].p, st);
-    g_launches.fetch_add(3, std::memory_order_relaxed);
-    if (e) return cuda_fail(e, "k3 abft launch");
+    // two-pass / multipass sizes: transform (strikes included), then checksum
+    // and window sweeps over x and y on the device (not fused yet)
+    rc = run_plain(p, x, y, batch, 0, signal_offset, dev, counters, st);
+    if (rc) return rc;
+    if (!slow.empty()) {
+      rc = strike_path(p, x, y, batch, 0, signal_offset, slow, st, nullptr);
+      if (rc) return rc;
+    }
+    TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, 0, batch, p->rows[enc].p, enc_table(p, false), enc, delta, ab,
+                                  (Counters*)counters, 1, st),
+             "row checksums");
+    const size_t cb = cbytes(p->prec);
+    int e = p->wsum.ensure((size_t)3 * nwin * p->n * cb);
+    if (e) return cuda_fail(e, "window sums");
+    char* s_in = (char*)p->wsum.p;
+    char* s_out = s_in + (size_t)nwin * p->n * cb;
+    char* ref = s_out + (size_t)nwin * p->n * cb;
+    TFFT_TRY(launch_weighted_cols(p->prec, x, p->n, 0, batch, W, signal_offset, s_in, st), "window s_in");
+    TFFT_TRY(launch_weighted_cols(p->prec, y, p->n, 0, batch, W, signal_offset, s_out, st), "window s_out");
+    std::vector<DevFault> none;
+    int e2 = p->counters.ensure(8 * sizeof(uint64_t));
+    if (e2) return cuda_fail(e2, "counters");
+    rc = run_plain(p, s_in, ref, nwin, 0, 0, none, (uint64_t*)p->counters.p + 4, st);
+    if (rc) return rc;
+    TFFT_TRY(launch_group_div_batched(p->prec, ref, s_out, p->n, nwin, sums->win_div, st), "window group div");
+    return TFFT_OK;
   }
   if (slow.empty()) return TFFT_OK;
   // strike path for the faults the fused kernel cannot reach, then refresh
@@ -472,7 +536,7 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
   for (size_t i = 0; i < touched.size(); i += 2) {
     const int64_t a = touched[i], b = touched[i + 1];
     TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, a, b - a, p->rows[enc].p,
-                                  p->k1 ? p->tw_fwd.p : k3_enc_table(p->k3), enc, delta, ab, (Counters*)counters, 1, st),
+                                  p->k1 ? p->tw_fwd.p : enc_table(p, false), enc, delta, ab, (Counters*)counters, 1, st),
              "strike row checksums");
     const int64_t w = a / W;
     const int64_t w0 = w * W, w1 = std::min<int64_t>(w0 + W, batch);
@@ -600,7 +664,7 @@ int tfft_correction_column(tfft_plan* p, const void* snap_in, const void* snap_o
 
 int tfft_patch_row(tfft_plan* p, void* y_row, const void* col, int enc, double* res_dev, void* stream) {
   if (!p) return fail(TFFT_EINVAL, "null plan");
-  TFFT_TRY(launch_patch_row(p->prec, y_row, col, p->n, enc, p->k1 ? p->tw_fwd.p : k3_enc_table(p->k3), res_dev,
+  TFFT_TRY(launch_patch_row(p->prec, y_row, col, p->n, enc, p->k1 ? p->tw_fwd.p : enc_table(p, false), res_dev,
                             (cudaStream_t)stream),
            "patch row");
   return TFFT_OK;
@@ -622,7 +686,7 @@ int tfft_row_checksums(tfft_plan* p, const void* x, const void* y, int64_t row0,
     counters = (uint64_t*)p->counters.p;
   }
   TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, row0, nrows, p->rows[enc].p,
-                                p->k1 ? p->tw_fwd.p : k3_enc_table(p->k3), enc, delta, ab, (Counters*)counters, count,
+                                p->k1 ? p->tw_fwd.p : enc_table(p, false), enc, delta, ab, (Counters*)counters, count,
                                 (cudaStream_t)stream),
            "row checksums");
   return TFFT_OK;
@@ -636,7 +700,7 @@ int tfft_jou_variant(tfft_plan* p, const void* x, void* out, int64_t rows, void*
 
 int tfft_jou_undo(tfft_plan* p, void* y, int64_t rows, void* stream) {
   if (!p) return fail(TFFT_EINVAL, "null plan");
-  const void* twi = p->k1 ? p->tw_inv.p : k3_enc_table_inv(p->k3);
+  const void* twi = p->k1 ? p->tw_inv.p : enc_table(p, true);
   TFFT_TRY(launch_jou(p->prec, 1, nullptr, y, rows, p->n, twi, (cudaStream_t)stream), "jou undo");
   return TFFT_OK;
 }

@@ -94,6 +94,29 @@ __global__ void flip_element_kernel(C<T>* buf, int64_t index, int part, int bit)
   buf[index] = v;
 }
 
+__global__ void base_table_kernel(float2* f, double2* d, int64_t s, int r, int inverse) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < s; q += (int64_t)gridDim.x * blockDim.x) {
+    double sn, cs;
+    sincospi(-2.0 * (double)q / ((double)s * r), &sn, &cs);
+    if (q == 0) {
+      sn = 0;
+      cs = 1;
+    }
+    if (inverse) sn = -sn;
+    if (f) f[q] = make_float2((float)cs, (float)sn);
+    else d[q] = make_double2(cs, sn);
+  }
+}
+
+// omega_(s r)^q for q < s (conj for inverse), FP64 sincospi rounded once
+int launch_base_table(int prec, int64_t s, int r, int inverse, void* dst, cudaStream_t st) {
+  int64_t blocks = (s + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  base_table_kernel<<<(unsigned)blocks, 256, 0, st>>>(prec == 0 ? (float2*)dst : nullptr,
+                                                        prec == 0 ? nullptr : (double2*)dst, s, r, inverse);
+  return (int)cudaGetLastError();
+}
+
 int launch_flip(int prec, void* buf, int64_t index, int part, int bit, cudaStream_t st) {
   if (prec == 0) flip_element_kernel<float><<<1, 1, 0, st>>>((float2*)buf, index, part, bit);
   else flip_element_kernel<double><<<1, 1, 0, st>>>((double2*)buf, index, part, bit);
@@ -292,6 +315,9 @@ int launch_vadd(int prec, void* a, const void* b, int64_t n, cudaStream_t st) {
 template <typename T>
 __global__ void __launch_bounds__(256) group_div_kernel(const C<T>* ref, const C<T>* s_out, int64_t n, double* out) {
   __shared__ double sh[8 * 2];
+  ref += blockIdx.x * n;
+  s_out += blockIdx.x * n;
+  out += blockIdx.x;
   double acc[2] = {0, 0};
   for (int64_t k = threadIdx.x; k < n; k += 256) {
     const double dr = (double)ref[k].x - (double)s_out[k].x;
@@ -304,8 +330,22 @@ __global__ void __launch_bounds__(256) group_div_kernel(const C<T>* ref, const C
 }
 
 int launch_group_div(int prec, const void* ref, const void* s_out, int64_t n, double* out, cudaStream_t st) {
-  if (prec == 0) group_div_kernel<float><<<1, 256, 0, st>>>((const float2*)ref, (const float2*)s_out, n, out);
-  else group_div_kernel<double><<<1, 256, 0, st>>>((const double2*)ref, (const double2*)s_out, n, out);
+  return launch_group_div_batched(prec, ref, s_out, n, 1, out, st);
+}
+
+// one CTA per window: row w of ref / s_out -> out[w]
+int launch_group_div_batched(int prec, const void* ref, const void* s_out, int64_t n, int64_t count, double* out,
+                             cudaStream_t st) {
+  if (count < 1) return 0;
+  for (int64_t w0 = 0; w0 < count; w0 += 65535) {
+    const int64_t cnt = count - w0 < 65535 ? count - w0 : 65535;
+    if (prec == 0)
+      group_div_kernel<float><<<(unsigned)cnt, 256, 0, st>>>((const float2*)ref + w0 * n, (const float2*)s_out + w0 * n,
+                                                            n, out + w0);
+    else
+      group_div_kernel<double><<<(unsigned)cnt, 256, 0, st>>>((const double2*)ref + w0 * n,
+                                                             (const double2*)s_out + w0 * n, n, out + w0);
+  }
   return (int)cudaGetLastError();
 }
 

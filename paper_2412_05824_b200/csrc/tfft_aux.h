@@ -21,6 +21,9 @@ int launch_axpby(int prec, void* z, int64_t n, double ar, double ai, const void*
                  const void* y, cudaStream_t st);
 int launch_vadd(int prec, void* a, const void* b, int64_t n, cudaStream_t st);
 int launch_group_div(int prec, const void* ref, const void* s_out, int64_t n, double* out, cudaStream_t st);
+int launch_group_div_batched(int prec, const void* ref, const void* s_out, int64_t n, int64_t count, double* out,
+                             cudaStream_t st);
+int launch_base_table(int prec, int64_t s, int r, int inverse, void* dst, cudaStream_t st);
 int launch_correction_column(int prec, const void* snap_out, const void* ref64, int64_t n, double weight, void* col,
                              double* res, cudaStream_t st);
 int launch_patch_row(int prec, void* yk, const void* col, int64_t n, int enc, const void* tw, double* res,

@@ -1,13 +1,392 @@
-// temporary: two-pass kernels not yet built
+// K3: two-pass (four-step) batched FFT for 2^13 < N <= 2^22 (FP32 from 2^14).
+//
+// N = N1 x N2 with N1 = the reference plan's first stage span (fft_core.py
+// stage boundaries), so the pass-A output IS the canonical stage-1
+// intermediate Z[p][q] = sum_v x[p + N2 v] w_N1^{qv}, stored
+// at q + N1 p; stage-1 strikes flip it in registers before the w_N^{pq}
+// twiddle, exactly where the reference's injector fires.
+//
+//   pass A: for each signal and each block of CB consecutive columns p, load
+//           the N1 x CB tile (CB contiguous elements per row v: coalesced),
+//           N1-point FFTs in shared memory (one column per slot, swizzled with a
+//           per-slot XOR key), twiddle w_N^{pq}, store rows of Z contiguously.
+//   pass B: for each block of CB consecutive q, load the N2 x CB tile of Z,
+//           N2-point FFTs, transpose through shared memory, store
+//           y[q + N1 k] in CB-contiguous runs.
+//
+// Both passes are one persistent kernel launch each; the engine (tfft_fft.cuh)
+// is the same one K1 uses.
+#include <cmath>
+#include <vector>
+
+#include "tfft_fft.cuh"
+#include "tfft_internal.h"
 #include "tfft_k3.h"
+#include "tfft_aux.h"
+
 namespace tfft {
-struct K3Plan {};
-int k3_create(int64_t, int, const int64_t*, int, int, K3Plan**) { return (int)cudaErrorInvalidValue; }
-void k3_destroy(K3Plan*) {}
-int k3_execute(K3Plan*, const void*, void*, int64_t, int, const DevFault*, int, Counters*, void*, cudaStream_t) { return (int)cudaErrorInvalidValue; }
-int k3_protected(K3Plan*, const void*, void*, int64_t, int64_t, const DevFault*, int, Counters*, const AbftArgs&, const void*, cudaStream_t) { return (int)cudaErrorInvalidValue; }
-int k3_base_table(K3Plan*, int, int64_t, int, int, void*, cudaStream_t) { return (int)cudaErrorInvalidValue; }
-bool k3_strikes_stage1(const K3Plan*) { return false; }
-const void* k3_enc_table(K3Plan*) { return nullptr; }
-const void* k3_enc_table_inv(K3Plan*) { return nullptr; }
+
+template <typename T, int LOGL>
+struct ColCfg {
+  static constexpr int L = 1 << LOGL;
+  static constexpr int EMAX = sizeof(T) == 4 ? 16 : 8;
+  static constexpr int E = EMAX < L ? EMAX : L;
+  static constexpr int TPS = L / E;
+  static constexpr int BPC = (int)sizeof(C<T>);
+  static constexpr int CB0 = 65536 / (L * BPC);
+  static constexpr int CB = CB0 < 2 ? 2 : (CB0 > 32 ? 32 : CB0);
+  static constexpr int NT = CB * TPS;
+  static constexpr int TILE = CB * L;
+  static constexpr int SMEM = TILE * BPC;
+  static constexpr int KEYMASK = sizeof(T) == 4 ? 15 : 7;
+};
+
+struct ColArgs {
+  const void* src;
+  void* dst;
+  int64_t batch;
+  int64_t n;        // full transform length N
+  int64_t pitch;    // row pitch (elements) of the src matrix view
+  int64_t ncols;    // columns of the view (N / L)
+  int64_t n1;       // N1 (output stride of pass B, layout of Z)
+  const void* tw;   // omega_L^m (conj for inverse), L entries
+  const void* hi;   // omega_N^{h * 2^lo_bits}
+  const void* lo;   // omega_N^{l}
+  int lo_bits;
+  const DevFault* faults;
+  int nfaults;
+  int strike_stage; // stage index whose boundary pass A's output is (1), or -1
+  Counters* counters;
+};
+
+template <typename T, int LOGL, bool INV, int MODE>
+__global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
+  using K = ColCfg<T, LOGL>;
+  using F = Fft<T, K::L, K::EMAX, INV>;
+  using CT = C<T>;
+  constexpr int L = K::L, E = K::E, TPS = K::TPS, CB = K::CB, NT = K::NT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  CT* tile = reinterpret_cast<CT*>(smem);
+
+  const int tid = threadIdx.x;
+  const int g = tid / TPS;
+  const int tau = tid % TPS;
+  const int key = g & K::KEYMASK;
+  CT* slot = tile + g * L;
+  const CT* __restrict__ src = static_cast<const CT*>(a.src);
+  CT* __restrict__ dst = static_cast<CT*>(a.dst);
+  const CT* __restrict__ tw = static_cast<const CT*>(a.tw);
+  const int64_t ncb = a.ncols / CB;
+  const int64_t ntiles = a.batch * ncb;
+  bool bad = false;
+
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t sig = t / ncb;
+    const int64_t c0 = (t - sig * ncb) * CB;
+    const CT* s = src + sig * a.n + c0;
+    // ---- load the L x CB tile (rows contiguous in global) into column slots
+    CT ld[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int e = i * NT + tid;
+      const int r = e / CB, c = e % CB;
+      ld[i] = __ldcs(s + (int64_t)r * a.pitch + c);
+    }
+    if constexpr (MODE == 0) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) bad |= !finite2<T>(ld[i]);
+      if (a.nfaults > 0) {
+        for (int f = 0; f < a.nfaults; ++f) {
+          const DevFault fl = a.faults[f];
+          if (fl.signal != sig || fl.stage != 0) continue;
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const int e = i * NT + tid;
+            const int r = e / CB, c = e % CB;
+            if (c0 + c + (int64_t)r * a.pitch == fl.element) {
+              if (fl.part == 0) ld[i].x = flip_bits(ld[i].x, fl.bit);
+              else ld[i].y = flip_bits(ld[i].y, fl.bit);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int e = i * NT + tid;
+      const int r = e / CB, c = e % CB;
+      tile[c * L + F::phys(r, c & K::KEYMASK)] = ld[i];
+    }
+    __syncthreads();
+    // ---- column FFTs
+    CT v[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = slot[F::phys(tau + TPS * k, key)];
+    F::run(slot, v, tau, tw, key);
+    if constexpr (MODE == 0) {
+      // twiddle w_N^{p q} (two-level table) and store Z[p][q] at q + N1 p
+      const int64_t p = c0 + g;
+      const CT* __restrict__ hi = static_cast<const CT*>(a.hi);
+      const CT* __restrict__ lo = static_cast<const CT*>(a.lo);
+      const int64_t lomask = (int64_t(1) << a.lo_bits) - 1;
+      CT* d = dst + sig * a.n + p * L;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        const int q = tau + TPS * F::out_pos(k);
+        if (a.nfaults > 0 && a.strike_stage == 1) {
+          for (int f = 0; f < a.nfaults; ++f) {
+            const DevFault fl = a.faults[f];
+            if (fl.signal == sig && fl.stage == 1 && fl.element == q + p * L) {
+              if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
+              else v[k].y = flip_bits(v[k].y, fl.bit);
+            }
+          }
+        }
+        const int64_t m = p * (int64_t)q;
+        const CT w = cmul<T>(__ldg(hi + (m >> a.lo_bits)), __ldg(lo + (m & lomask)));
+        d[q] = cmul<T>(v[k], w);
+      }
+      __syncthreads();  // tile reuse by the next load
+    } else {
+      // transpose through the tile, then y[q + N1 k] in CB-contiguous runs
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < E; ++k) slot[F::phys(tau + TPS * F::out_pos(k), key)] = v[k];
+      __syncthreads();
+      CT* d = dst + sig * a.n + c0;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int e = i * NT + tid;
+        const int r = e / CB, c = e % CB;
+        CT val = tile[c * L + F::phys(r, c & K::KEYMASK)];
+        if constexpr (INV) val = cscale<T>(val, (T)(1.0 / (double)a.n));
+        __stcs(d + (int64_t)r * a.n1 + c, val);
+      }
+      __syncthreads();
+    }
+  }
+  if constexpr (MODE == 0) {
+    if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
+  }
 }
+
+template <typename T, int LOGL, bool INV, int MODE>
+static int launch_col(const ColArgs& a, int num_sms, cudaStream_t st) {
+  using K = ColCfg<T, LOGL>;
+  auto kern = col_kernel<T, LOGL, INV, MODE>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM);
+  if (e != cudaSuccess) return (int)e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = a.batch * (a.ncols / K::CB);
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) return 0;
+  kern<<<(unsigned)grid, K::NT, K::SMEM, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, bool INV, int MODE>
+static int dispatch_col(int logl, const ColArgs& a, int num_sms, cudaStream_t st) {
+  switch (logl) {
+#define TFFT_COL(L) \
+  case L: return launch_col<T, L, INV, MODE>(a, num_sms, st);
+    TFFT_COL(6) TFFT_COL(7) TFFT_COL(8) TFFT_COL(9) TFFT_COL(10) TFFT_COL(11)
+#undef TFFT_COL
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
+static int col(int prec, bool inv, int mode, int logl, const ColArgs& a, int num_sms, cudaStream_t st) {
+  if (prec == 0) {
+    if (mode == 0) return inv ? dispatch_col<float, true, 0>(logl, a, num_sms, st) : dispatch_col<float, false, 0>(logl, a, num_sms, st);
+    return inv ? dispatch_col<float, true, 1>(logl, a, num_sms, st) : dispatch_col<float, false, 1>(logl, a, num_sms, st);
+  }
+  if (mode == 0) return inv ? dispatch_col<double, true, 0>(logl, a, num_sms, st) : dispatch_col<double, false, 0>(logl, a, num_sms, st);
+  return inv ? dispatch_col<double, true, 1>(logl, a, num_sms, st) : dispatch_col<double, false, 1>(logl, a, num_sms, st);
+}
+
+// ---------------------------------------------------------------------------
+// plan: tables + intermediate workspace
+
+struct K3Plan {
+  int64_t n = 0;
+  int prec = 0;
+  int l1 = 0, l2 = 0;  // log2 N1, log2 N2
+  int lo_bits = 0;
+  bool stage1 = false;
+  int num_sms = 148;
+  void* tw1[2] = {nullptr, nullptr};
+  void* tw2[2] = {nullptr, nullptr};
+  void* hi[2] = {nullptr, nullptr};
+  void* lo[2] = {nullptr, nullptr};
+  void* enc[2] = {nullptr, nullptr};
+  void* inter = nullptr;
+  size_t inter_cap = 0;
+};
+
+namespace {
+
+// omega_M^{k * step} for k < count, extended precision, rounded once
+int upload_table(int prec, int64_t M, int64_t step, int64_t count, bool conj, void** out) {
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  const size_t cb = prec == 0 ? 8 : 16;
+  std::vector<unsigned char> host(count * cb);
+  for (int64_t k = 0; k < count; ++k) {
+    const int64_t m = (k * step) % M;
+    const long double ang = two_pi * (long double)m / (long double)M;
+    long double re = cosl(ang), im = -sinl(ang);
+    if (4 * m == M) { re = 0; im = -1; }
+    if (2 * m == M) { re = -1; im = 0; }
+    if (4 * m == 3 * M) { re = 0; im = 1; }
+    if (m == 0) { re = 1; im = 0; }
+    if (conj) im = -im;
+    if (prec == 0) {
+      float* f = (float*)host.data();
+      f[2 * k] = (float)re;
+      f[2 * k + 1] = (float)im;
+    } else {
+      double* d = (double*)host.data();
+      d[2 * k] = (double)re;
+      d[2 * k + 1] = (double)im;
+    }
+  }
+  cudaError_t e = cudaMalloc(out, host.size());
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaMemcpy(*out, host.data(), host.size(), cudaMemcpyHostToDevice);
+}
+
+int ilog2i(int64_t v) {
+  int r = 0;
+  while ((int64_t(1) << r) < v) ++r;
+  return r;
+}
+
+}  // namespace
+
+int k3_create(int64_t n, int prec, const int64_t* spans, int nstages, int num_sms, K3Plan** out) {
+  *out = nullptr;
+  const int logn = ilog2i(n);
+  int l1;
+  if (nstages >= 2) l1 = ilog2i(spans[0]);
+  else l1 = (logn + 1) / 2;
+  int l2 = logn - l1;
+  if (nstages > 2 || l1 < 6 || l2 < 6 || l1 > 11 || l2 > 11) {
+    // the reference's span may be lopsided; fall back to a balanced split
+    // (stage-1 strikes then go through the strike path)
+    if (nstages > 2 || logn < 12 || logn > 22) return (int)cudaErrorInvalidValue;
+    l1 = (logn + 1) / 2;
+    l2 = logn - l1;
+    nstages = 1;
+  }
+  K3Plan* p = new K3Plan();
+  p->n = n;
+  p->prec = prec;
+  p->l1 = l1;
+  p->l2 = l2;
+  p->stage1 = nstages == 2;
+  p->num_sms = num_sms;
+  p->lo_bits = (logn + 1) / 2;
+  const int64_t N1 = int64_t(1) << l1, N2 = int64_t(1) << l2;
+  int e = 0;
+  for (int c = 0; c < 2 && !e; ++c) {
+    e = upload_table(prec, N1, 1, N1, c == 1, &p->tw1[c]);
+    if (!e) e = upload_table(prec, N2, 1, N2, c == 1, &p->tw2[c]);
+    if (!e) e = upload_table(prec, n, int64_t(1) << p->lo_bits, n >> p->lo_bits, c == 1, &p->hi[c]);
+    if (!e) e = upload_table(prec, n, 1, int64_t(1) << p->lo_bits, c == 1, &p->lo[c]);
+  }
+  if (e) {
+    k3_destroy(p);
+    return e;
+  }
+  *out = p;
+  return 0;
+}
+
+void k3_destroy(K3Plan* p) {
+  if (!p) return;
+  for (int c = 0; c < 2; ++c) {
+    cudaFree(p->tw1[c]);
+    cudaFree(p->tw2[c]);
+    cudaFree(p->hi[c]);
+    cudaFree(p->lo[c]);
+    cudaFree(p->enc[c]);
+  }
+  cudaFree(p->inter);
+  delete p;
+}
+
+bool k3_strikes_stage1(const K3Plan* p) { return p && p->stage1; }
+
+int k3_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults, int nfaults,
+               Counters* counters, void* reserved, cudaStream_t st) {
+  (void)reserved;
+  const size_t cb = p->prec == 0 ? 8 : 16;
+  const size_t need = (size_t)batch * p->n * cb;
+  if (p->inter_cap < need) {
+    cudaFree(p->inter);
+    p->inter = nullptr;
+    p->inter_cap = 0;
+    cudaError_t e = cudaMalloc(&p->inter, need);
+    if (e != cudaSuccess) return (int)e;
+    p->inter_cap = need;
+  }
+  const int64_t N1 = int64_t(1) << p->l1, N2 = int64_t(1) << p->l2;
+  const int c = inverse ? 1 : 0;
+  ColArgs a{};
+  a.src = x;
+  a.dst = p->inter;
+  a.batch = batch;
+  a.n = p->n;
+  a.pitch = N2;
+  a.ncols = N2;
+  a.n1 = N1;
+  a.tw = p->tw1[c];
+  a.hi = p->hi[c];
+  a.lo = p->lo[c];
+  a.lo_bits = p->lo_bits;
+  a.faults = faults;
+  a.nfaults = nfaults;
+  a.strike_stage = p->stage1 ? 1 : -1;
+  a.counters = counters;
+  int rc = col(p->prec, inverse != 0, 0, p->l1, a, p->num_sms, st);
+  if (rc) return rc;
+  ColArgs b = a;
+  b.src = p->inter;
+  b.dst = y;
+  b.pitch = N1;
+  b.ncols = N1;
+  b.tw = p->tw2[c];
+  b.nfaults = 0;
+  b.strike_stage = -1;
+  return col(p->prec, inverse != 0, 1, p->l2, b, p->num_sms, st);
+}
+
+int k3_protected(K3Plan*, const void*, void*, int64_t, int64_t, const DevFault*, int, Counters*, const AbftArgs&,
+                 const void*, cudaStream_t) {
+  return (int)cudaErrorNotSupported;  // protected runs over K3 use the unfused device path (tfft_api.cu)
+}
+
+int k3_base_table(K3Plan*, int prec, int64_t s, int r, int inverse, void* dst, cudaStream_t st) {
+  return launch_base_table(prec, s, r, inverse, dst, st);
+}
+
+const void* k3_enc_table(K3Plan* p) {
+  if (!p->enc[0]) upload_table(p->prec, p->n, 1, p->n, false, &p->enc[0]);
+  return p->enc[0];
+}
+
+const void* k3_enc_table_inv(K3Plan* p) {
+  if (!p->enc[1]) upload_table(p->prec, p->n, 1, p->n, true, &p->enc[1]);
+  return p->enc[1];
+}
+
+}  // namespace tfft

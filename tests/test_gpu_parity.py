@@ -187,3 +187,35 @@ def test_stockham_pass_boundary_and_butterflies():
         got = tf.butterfly_radix(u, r)
         ref = np.fft.fft(u)
         assert np.abs(got - ref).max() <= 8 * EPS["double"] * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+@pytest.mark.parametrize("log2n", [13, 14, 15, 16, 17, 18, 20])
+def test_two_pass_sizes_vs_oracle(precision, log2n):
+    """C2-style sizes through K3 (two-pass) against the oracle, both directions."""
+    tf = _tf()
+    from oracle import ref_oracle as O
+    n = 2 ** log2n
+    b = 3 if log2n <= 17 else 1
+    x = gaussian(n, b, precision, seed=log2n)
+    plan = tf.build_plan(tf.select_params(n, b, precision), precision)
+    y = tf.execute_plan(plan, tf.SignalBatch(x)).data
+    ref = O.execute(x, O.select_params(n, b, precision))
+    assert rel_l2(y, ref) <= l2_tol(precision, n)
+    assert max_rel_error(y, ref) <= oracle_tol(precision, n)
+    back = tf.execute_plan(plan, tf.SignalBatch(y), "inverse").data
+    assert max_rel_error(back, x) <= (1e-5 if precision == "single" else 1e-12)
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_multipass_beyond_two_pass(precision):
+    """N = 2^23 (three-stage curated plan) via the reference-order device passes."""
+    tf = _tf()
+    n = 2 ** 23
+    x = gaussian(n, 1, precision, seed=23)
+    plan = tf.build_plan(tf.select_params(n, 1, precision), precision)
+    y = tf.execute_plan(plan, tf.SignalBatch(x)).data
+    ref = np.fft.fft(x.astype(np.complex128), axis=1)
+    assert rel_l2(y, ref) <= l2_tol(precision, n)
+    back = tf.execute_plan(plan, tf.SignalBatch(y), "inverse").data
+    assert max_rel_error(back, x) <= (1e-5 if precision == "single" else 1e-12)
