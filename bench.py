@@ -1,0 +1,434 @@
+#!/usr/bin/env python3
+"""Benchmark for the B200 batched FFT (+ fused ABFT) — the driver's contract.
+
+    python bench.py --gpus N --steps K --warmup W [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Headline workload (BASELINE.json configs[1], "C2"): FP64 complex 1-D forward
+FFT sweep N = 2^8 .. 2^20, each with B = 2^26 / N signals (1 GiB in, 1 GiB
+out, both larger than the 126 MB L2, so no flush is needed). One step = the
+13 transforms of the sweep. ``value`` = algorithmic GFLOP/s (5 N log2 N per
+transform) over the whole job (all ranks), inputs resident in HBM; ``e2e`` =
+the same metric through the public API (execute_plan on pinned host numpy
+batches: H2D + kernels + D2H inside the timed region). Weak scaling: every
+rank transforms its own 1 GiB shard per N; no data crosses NVLink.
+
+Extra keys: per-N GB/s and roofline fractions, the fused-ABFT overhead on
+C3 (N = 4096, 1 GiB, T = 8) and C5 (N = 2^16, 2048 signals/GPU, T = 8, with
+the NCCL fault-counter all-reduce when N > 1), clocks sampled during the
+timed region, the dominant kernel's roofline, and the reference CPU path
+timed on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOP = lambda n: 5.0 * n * np.log2(n)  # noqa: E731
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--sweep", default="8-20", help="log2 N range of the C2 sweep")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-abft", action="store_true")
+    ap.add_argument("--cpu-fraction", type=float, default=0.25,
+                    help="fraction of each N's batch the CPU baseline transforms")
+    return ap.parse_args()
+
+
+def sweep_sizes(spec):
+    a, b = (int(v) for v in spec.split("-"))
+    return [2 ** k for k in range(a, b + 1)]
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, device_backend=True):
+        import torch
+        import torch.distributed as dist
+
+        if device_backend:
+            torch.cuda.set_device(self.local)
+        if self.world > 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("nccl" if device_backend else "gloo")
+            self.pg = dist
+        return self
+
+    def barrier(self):
+        if self.pg is not None:
+            self.pg.barrier()
+
+    def max(self, v):
+        if self.pg is None:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v):
+        if self.pg is None:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_rank{index}.csv"
+
+    def start(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.path.read_text().splitlines():
+            f = [v.strip() for v in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def run_ours(args, dist):
+    import torch
+
+    import paper_2412_05824_b200 as tf
+    from paper_2412_05824_b200 import _lib, abft as A, fft_core
+
+    lib = _lib.load()
+    sizes = sweep_sizes(args.sweep)
+    total_elems = 2 ** 26  # 1 GiB of complex128 per rank per N
+    x = torch.randn(total_elems * 2, dtype=torch.float64, device="cuda").view(torch.complex128)
+    y = torch.empty_like(x)
+    plans = {n: tf.build_plan(tf.select_params(n, total_elems // n, "double"), "double") for n in sizes}
+    for n in sizes:  # plan creation (twiddle upload) outside the timed region
+        fft_core.device_execute(plans[n], x.view(-1, n)[:1], y.view(-1, n)[:1])
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+
+    def step(events=None):
+        for i, n in enumerate(sizes):
+            if events is not None:
+                events[i][0].record(stream)
+            fft_core.device_execute(plans[n], x.view(-1, n), y.view(-1, n))
+            if events is not None:
+                events[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    per_n = [[] for _ in sizes]
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in sizes]
+          for _ in range(args.steps)]
+    clocks = Clocks(dist.local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.tfft_launch_count()
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in range(args.steps):
+        step(ev[s])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    launches = lib.tfft_launch_count() - launches0
+    elapsed = t0.elapsed_time(t1) / 1e3
+    for s in range(args.steps):
+        for i in range(len(sizes)):
+            per_n[i].append(ev[s][i][0].elapsed_time(ev[s][i][1]) / 1e3)
+    elapsed = dist.max(elapsed)
+    flops_rank = sum(FLOP(n) * (total_elems // n) for n in sizes)
+    value = flops_rank * dist.world * args.steps / elapsed / 1e9
+    peak, peak_src = peaks()
+    sweep = []
+    for i, n in enumerate(sizes):
+        t = statistics.median(per_n[i])
+        b = total_elems // n
+        gbs = 2 * n * b * 16 / t / 1e9
+        sweep.append({"n": n, "batch": b, "ms": round(t * 1e3, 4), "gflops": round(FLOP(n) * b / t / 1e9, 1),
+                      "gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
+                      "kernel": "k1_single_pass" if n <= 4096 else "k3_two_pass"})
+    dom = max(range(len(sizes)), key=lambda i: statistics.mean(per_n[i]))
+    dn = sweep[dom]
+    roofline = {"bound": "hbm", "achieved": dn["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": round(dn["gbs"] / peak, 4), "traffic": None,
+                "kernel": f"{dn['kernel']} (N={dn['n']}, B={dn['batch']})",
+                "algorithmic_bytes_per_launch": 2 * dn["n"] * dn["batch"] * 16,
+                "peak_source": peak_src}
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        tr = json.loads(prof.read_text()).get(str(dn["n"]))
+        if tr:
+            roofline["traffic"] = tr
+
+    out = {
+        "metric": "FFT GFLOP/s (5 N log2 N per transform), C2 FP64 sweep N=2^8..2^20",
+        "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic (torch.randn)",
+        "config": {"workload": "C2: FP64 complex 1-D forward FFT, N=2^8..2^20, B=2^26/N (1 GiB in per N per GPU)",
+                   "transforms_per_step": len(sizes), "bytes_per_step_per_gpu": 2 * total_elems * 16 * len(sizes),
+                   "l2": "inputs 1 GiB > 126 MB L2 (no flush needed)", "parallelism": f"batch-shard x{dist.world}"},
+        "gb_per_s": round(2 * total_elems * 16 * len(sizes) * dist.world * args.steps / elapsed / 1e9, 1),
+        "sweep": sweep, "roofline": roofline, "clocks": clk, "gpu_launches": int(launches),
+    }
+    del x, y
+    torch.cuda.empty_cache()
+    if not args.no_abft:
+        out["abft"] = abft_overheads(args, dist)
+    if not args.no_e2e:
+        out["e2e"] = e2e(args, dist, sizes, plans, total_elems)
+    return out
+
+
+def _time_loop(fn, steps, warmup, dist):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    return dist.max(a.elapsed_time(b) / 1e3 / steps)
+
+
+def abft_overheads(args, dist):
+    """Fused two-sided ABFT overhead: C3 (N=4096) and C5 (N=2^16) at T=8."""
+    import torch
+
+    import paper_2412_05824_b200 as tf
+    from paper_2412_05824_b200 import abft as A, fft_core
+
+    res = {}
+    cases = [("C3_fp32_n4096", 4096, 32768, "single", 8), ("C3_fp64_n4096", 4096, 16384, "double", 8),
+             ("C5_fp32_n65536", 65536, 2048, "single", 8)]
+    for name, n, b, prec, T in cases:
+        dt = torch.complex64 if prec == "single" else torch.complex128
+        rdt = torch.float32 if prec == "single" else torch.float64
+        x = torch.randn(b * n * 2, dtype=rdt, device="cuda").view(dt).view(b, n)
+        y = torch.empty_like(x)
+        plan = tf.build_plan(tf.select_params(n, b, prec), prec)
+        ntx = -(-b // plan.bs)
+        nwin = -(-ntx // T)
+        sums = A._DeviceSums(b, nwin)
+        ctr = fft_core._Counters()
+        delta = A.default_delta(prec)
+        offset = dist.rank * b  # global signal indices of this shard (weights w_j = j + 1)
+        red = torch.zeros(4, dtype=torch.int64, device="cuda")
+
+        def plain():
+            fft_core.device_execute(plan, x, y)
+
+        def fused():
+            A.protected_device(plan, x, y, delta=delta, group_size=T, counters=ctr, sums=sums,
+                               signal_offset=offset)
+            if dist.pg is not None:  # K7: the only collective — fault counters over NVLink
+                red.copy_(ctr.dev)
+                dist.pg.all_reduce(red)
+
+        steps = max(args.steps, 5)
+        tp = _time_loop(plain, steps, args.warmup, dist)
+        tfz = _time_loop(fused, steps, args.warmup, dist)
+        gbs = 2 * n * b * (8 if prec == "single" else 16) / tp / 1e9
+        res[name] = {"n": n, "batch_per_gpu": b, "T": T, "bs": plan.bs, "plain_ms": round(tp * 1e3, 4),
+                     "fused_ms": round(tfz * 1e3, 4), "overhead_pct": round(100 * (tfz / tp - 1), 2),
+                     "plain_gbs": round(gbs, 1), "path": "fused K1+ABFT" if n <= 4096 else "K3 + device checksum sweeps"}
+        del x, y, sums
+        torch.cuda.empty_cache()
+    return res
+
+
+def e2e(args, dist, sizes, plans, total_elems):
+    """Public API with pinned host buffers: H2D + transform + D2H per N."""
+    import torch
+
+    import paper_2412_05824_b200 as tf
+
+    host_in = torch.randn(total_elems * 2, dtype=torch.float64).view(torch.complex128).pin_memory()
+    host_out = torch.empty(total_elems, dtype=torch.complex128).pin_memory()
+    xin, xout = host_in.numpy(), host_out.numpy()
+
+    def step():
+        for n in sizes:
+            tf.execute_plan(plans[n], tf.SignalBatch(xin.reshape(-1, n)), out=xout.reshape(-1, n))
+
+    steps = max(1, min(args.steps, 3))
+    step()  # warm-up (allocator, plan caches)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    el = dist.max((time.perf_counter() - t0) / steps)
+    flops = sum(FLOP(n) * (total_elems // n) for n in sizes) * dist.world
+    nbytes = total_elems * 16 * len(sizes)
+    return {"value": round(flops / el / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "steps": steps, "ms_per_step": round(el * 1e3, 2),
+            "path": "paper_2412_05824_b200.execute_plan(SignalBatch(pinned numpy), out=pinned numpy)"}
+
+
+# ---------------------------------------------------------------------------
+# the reference's CPU implementation (oracle/_ref compiled kernel, else the port)
+
+
+def cpu_reference(sizes, fraction, workers, steps=1, warmup=0):
+    from oracle import ref_oracle as O
+
+    kind = "reference" if O.use_ref_kernel(True) else "port"
+    total = 2 ** 26
+    rng = np.random.default_rng(1234)
+    batches = {}
+    for n in sizes:
+        b = max(1, int(total // n * fraction))
+        batches[n] = (rng.standard_normal((b, n)) + 1j * rng.standard_normal((b, n))).astype(np.complex128)
+    plans = {n: O.select_params(n, batches[n].shape[0], "double") for n in sizes}
+
+    def step():
+        for n in sizes:
+            O.execute(batches[n], plans[n], workers=workers)
+
+    for _ in range(warmup):
+        step()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    flops = sum(FLOP(n) * batches[n].shape[0] for n in sizes)
+    sample = (f"C2 sweep N=2^{int(np.log2(sizes[0]))}..2^{int(np.log2(sizes[-1]))}, "
+              f"{fraction:g} of each 1 GiB batch (B=2^26/N*{fraction:g}), FP64, forward; "
+              f"resilient_fft execute_plan driver restated in oracle/ref_oracle.py")
+    return {"value": round(flops / t / 1e9, 3), "unit": "GFLOP/s", "cores": workers, "kind": kind,
+            "sample": sample, "seconds": round(t, 2)}
+
+
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return None
+    workers = os.cpu_count() or 1
+    sizes = sweep_sizes(args.sweep)
+    frac = min(args.cpu_fraction, 1.0 / 16)
+    cb = cpu_reference(sizes, frac, workers, steps=args.steps, warmup=min(args.warmup, 1))
+    return {
+        "metric": "FFT GFLOP/s (5 N log2 N per transform), C2 FP64 sweep N=2^8..2^20",
+        "value": cb["value"], "unit": "GFLOP/s", "impl": "reference", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(cb["seconds"] * 1e3, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic (numpy normal)",
+        "config": {"workload": "C2: FP64 complex 1-D forward FFT, N=2^8..2^20 (bounded CPU sample)",
+                   "parallelism": f"host threads x{workers}"},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    if args.impl == "reference":
+        out = run_reference(args, dist)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return 0
+    dist.init()
+    out = run_ours(args, dist)
+    if dist.rank == 0 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_reference(sweep_sizes(args.sweep), args.cpu_fraction, 1)
+    if dist.rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -123,6 +123,15 @@ def base_table(s, r, dtype):
     return t
 
 
+@functools.lru_cache(maxsize=256)
+def _plan_tables(s, r, dtype, inverse):
+    """Tables are built once per plan in the reference (make_twiddles)."""
+    t = base_table(s, r, np.dtype(dtype).type)
+    t = np.conj(t) if inverse else t
+    t.setflags(write=False)
+    return t
+
+
 # ---------------------------------------------------------------------------
 # one Stockham pass — _kernels_py.py:13-45 / _kernels.pyx:19-84
 
@@ -225,10 +234,7 @@ def transform_block(plan, precision, rows, inverse=False, faults=None, tx_index=
             strike(faults, tx_index, si, work, row0)
             while pi < len(passes) and passes[pi][2] == si:
                 s, r, _ = passes[pi]
-                base = base_table(s, r, dtype)
-                if inverse:
-                    base = np.conj(base)
-                _PASS(work, scratch, s, r, base, inverse)
+                _PASS(work, scratch, s, r, _plan_tables(s, r, np.dtype(dtype).str, inverse), inverse)
                 work, scratch = scratch, work
                 pi += 1
         if inverse:
@@ -241,14 +247,27 @@ def transactions(b, bs):
     return [(i, s, min(s + bs, b)) for i, s in enumerate(range(0, b, bs))]
 
 
-def execute(x, plan, inverse=False, faults=None):
-    """fft_core.py:296-329 (serial; the reference is worker-count invariant)."""
+def execute(x, plan, inverse=False, faults=None, workers=1):
+    """fft_core.py:296-329; ``workers`` > 1 uses a thread pool over
+    transactions like the reference (fft_core.py:321-326)."""
     precision = precision_of(x)
     if not np.all(np.isfinite(x.view(x.real.dtype))):
         raise ValueError("batch contains non-finite values")
     y = np.empty_like(x)
-    for i, a, b in transactions(x.shape[0], plan.bs):
+    txs = transactions(x.shape[0], plan.bs)
+
+    def run(tx):
+        i, a, b = tx
         y[a:b] = transform_block(plan, precision, x[a:b], inverse, faults, i, a)
+
+    if workers > 1 and len(txs) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            list(pool.map(run, txs))
+    else:
+        for tx in txs:
+            run(tx)
     return y
 
 

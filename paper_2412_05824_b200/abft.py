@@ -261,13 +261,13 @@ class _DeviceSums:
         return c_in, c_out, self.floors.cpu().numpy(), self.div.cpu().numpy()
 
 
-def _weighted_columns(plan, src, row0, row1, group):
-    """(ngroups, n) device table of sum_{j in group} (j+1) src_j (abft.py:668-677)."""
+def _weighted_columns(plan, src, row0, row1, group, weight0=0):
+    """(ngroups, n) device table of sum_{j in group} (weight0+j+1) src_j (abft.py:668-677)."""
     lib = _lib.load()
     t = _device.torch()
     ng = (row1 - row0 + group - 1) // group
     out = t.empty((max(ng, 1), plan.n), dtype=src.dtype, device=src.device)
-    rc = lib.tfft_weighted_columns(_prec(plan), src.data_ptr(), plan.n, row0, row1, group, 0, out.data_ptr(),
+    rc = lib.tfft_weighted_columns(_prec(plan), src.data_ptr(), plan.n, row0, row1, group, weight0, out.data_ptr(),
                                    _device.stream_handle())
     _lib.check(rc, "tfft_weighted_columns")
     return out
@@ -324,15 +324,20 @@ def _group_div(plan, s_in, s_out, scratch, res):
 class _ProtectedRun:
     """The serial decision replay of abft.py:342-551, vector state on the device."""
 
-    def __init__(self, plan, source, out, delta, group_size, enc_kind, stats, sums_host):
+    def __init__(self, plan, source, out, delta, group_size, enc_kind, stats, sums_host, sig_off=0,
+                 global_b=None):
         t = _device.torch()
         self.plan, self.source, self.out = plan, source, out
         self.delta, self.enc_kind, self.stats = delta, enc_kind, stats
         self.c_in, self.c_out, self.floors, self.div = sums_host
         b, n = int(source.shape[0]), plan.n
+        # a batch shard keeps the GLOBAL location weights and indices
+        self.sig_off = sig_off
+        self.tx_off = sig_off // plan.bs
+        self.global_b = global_b if global_b is not None else b
         self.state = ChecksumState(
             group_size=group_size,
-            weights=np.arange(1, b + 1, dtype=REAL_DTYPES[plan.precision]),
+            weights=np.arange(sig_off + 1, sig_off + b + 1, dtype=REAL_DTYPES[plan.precision]),
             s_in=t.zeros(n, dtype=source.dtype, device="cuda"),
             s_out=t.zeros(n, dtype=source.dtype, device="cuda"),
         )
@@ -355,7 +360,7 @@ class _ProtectedRun:
         self.stats.signal_sweeps += 2 * tx.size
         if tx.index in self.window_out_contribs:
             self.window_out_contribs[tx.index] = _weighted_columns(self.plan, self.out, tx.start, tx.stop,
-                                                                   tx.size)[0]
+                                                                   tx.size, self.sig_off)[0]
             acc = _device.torch().zeros_like(self.state.s_out)
             for v in self.window_out_contribs.values():
                 _vec_add(self.plan, acc, v)
@@ -364,7 +369,7 @@ class _ProtectedRun:
     def _apply_pending(self, tx_by_index, decontaminate):
         pending = self.state.pending
         self.state.pending = None
-        k = pending.signal
+        k = pending.signal - self.sig_off
         col = self._col
         if _correction(self.plan, pending, col, self._res):
             observed = _patch(self.plan, self.out[k], col, self.enc_kind, self._res)
@@ -421,19 +426,19 @@ class _ProtectedRun:
             tx_res = sum(res[gj] for gj in range(tx.start, tx.stop))
             tx_wres = sum(float(self.state.weights[gj]) * res[gj] for gj in range(tx.start, tx.stop))
         try:
-            decoded = locate(tx_wres, tx_res, batch=len(self.state.weights)) - 1
+            decoded = locate(tx_wres, tx_res, batch=self.global_b) - 1
         except Undecodable:
             decoded = None
         if len(triggered) > 1:
             for gj, _, div in triggered:
-                self.stats.events.append(DetectionEvent(tx.index, gj, div, None))
+                self.stats.events.append(DetectionEvent(tx.index + self.tx_off, gj + self.sig_off, div, None))
             if self.state.pending is not None:
                 self._apply_pending(tx_by_index, decontaminate=True)
             self._recompute_transaction(tx)
             self.window_uncorrectable = True
             return
         gj, local, div = triggered[0]
-        self.stats.events.append(DetectionEvent(tx.index, gj, div, decoded))
+        self.stats.events.append(DetectionEvent(tx.index + self.tx_off, gj + self.sig_off, div, decoded))
         if self.state.pending is not None:
             self._apply_pending(tx_by_index, decontaminate=False)
             self.state.s_in = t_in.clone()
@@ -441,8 +446,9 @@ class _ProtectedRun:
             self.window_out_contribs = {tx.index: t_out}
             self.window_tx_count = 1
         self.state.pending = _Pending(
-            signal=gj, weight=float(self.state.weights[gj]), snap_in=t_in, snap_out=t_out, tx_index=tx.index,
-            divergence=div, located=gj, reference=complex(self.c_in[gj]),
+            signal=gj + self.sig_off, weight=float(self.state.weights[gj]), snap_in=t_in, snap_out=t_out,
+            tx_index=tx.index,
+            divergence=div, located=gj + self.sig_off, reference=complex(self.c_in[gj]),
             floor=float(max(self.floors[gj], DIVERGENCE_FLOOR)))
 
     # -- verification boundaries (abft.py:493-551) ----------------------------
@@ -457,7 +463,7 @@ class _ProtectedRun:
             self._apply_pending(tx_by_index, decontaminate=True)
         group_div = _group_div(self.plan, state.s_in, state.s_out, self._ref, self._res)
         group_hit = group_div > self.delta
-        events = [e for e in self.stats.events if e.signal in state.residuals]
+        events = [e for e in self.stats.events if e.signal - self.sig_off in state.residuals]
         if group_hit and not events and not self.window_corrected and not self.window_uncorrectable:
             self.window_uncorrectable = True
         divergence = max([e.divergence for e in events] + ([group_div] if group_hit else []), default=group_div)
@@ -539,7 +545,7 @@ def _prepare(plan, batch, e_left, delta):
     kind = e_left.kind if isinstance(e_left, EncodingVector) else e_left
     if kind not in LEFT_KINDS:
         raise ValueError(f"left encoding must be one of {LEFT_KINDS}, got {kind!r}")
-    if precision == "single" and batch.b > MAX_SINGLE_WEIGHT:
+    if precision == "single" and batch.b > MAX_SINGLE_WEIGHT:  # sharded: checked on the global batch
         raise ValueError("location weights above 2^24 are not exact in single precision")
     enc = e_left if isinstance(e_left, EncodingVector) else make_encoding_vector(kind, batch.n, precision)
     return precision, delta, kind, enc
@@ -567,6 +573,12 @@ def run_protected(plan, batch, e_left="wang", delta=None, group_size=1, mode="fu
     Fault-free runs return outputs bitwise equal to ``execute_plan`` (the
     fused kernel runs the identical butterfly code) and untriggered reports.
     """
+    return _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, out, 0, None)
+
+
+def _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, out, sig_off, global_b):
+    """run_protected over a (possibly sharded) batch: rows are global signals
+    [sig_off, sig_off + b) of a global batch of ``global_b`` signals."""
     if group_size < 1:
         raise ValueError("group size must be >= 1")
     if mode not in ("fused", "per-transaction"):
@@ -581,10 +593,11 @@ def run_protected(plan, batch, e_left="wang", delta=None, group_size=1, mode="fu
     ntx = len(txs)
     nwin = (ntx + group_size - 1) // group_size
     sums = _DeviceSums(batch.b, nwin)
-    faults = injector._collect(0, ntx) if injector is not None else []
+    tx_off = sig_off // plan.bs
+    faults = injector._collect(tx_off, tx_off + ntx) if injector is not None else []
     counters = _Counters()
     protected_device(plan, source, y, kind=kind, delta=delta, group_size=group_size, faults=faults,
-                     counters=counters, sums=sums)
+                     counters=counters, sums=sums, signal_offset=sig_off)
     c = counters.read()
     if c["nonfinite"]:
         for f in faults:
@@ -605,7 +618,7 @@ def run_protected(plan, batch, e_left="wang", delta=None, group_size=1, mode="fu
                                            uncorrectable=g > delta, verification_index=w))
     else:
         host = sums.host()
-        run = _ProtectedRun(plan, source, y, delta, group_size, kind, stats, host)
+        run = _ProtectedRun(plan, source, y, delta, group_size, kind, stats, host, sig_off, global_b)
         tx_by_index = {tx.index: tx for tx in txs}
         div = host[3]
         with np.errstate(over="ignore", invalid="ignore"):
@@ -615,8 +628,8 @@ def run_protected(plan, batch, e_left="wang", delta=None, group_size=1, mode="fu
                 if not _FORCE_ENGINE and not bool((div[a:b] > delta).any()):
                     run.skip_clean_window(last - first, float(win_div[w]))
                     continue
-                t_in = _weighted_columns(plan, source, a, b, plan.bs)
-                t_out = _weighted_columns(plan, y, a, b, plan.bs)
+                t_in = _weighted_columns(plan, source, a, b, plan.bs, sig_off)
+                t_out = _weighted_columns(plan, y, a, b, plan.bs, sig_off)
                 for i, tx in enumerate(txs[first:last]):
                     run.feed(tx, t_in[i], t_out[i], tx_by_index)
             reports = run.finish(tx_by_index)
