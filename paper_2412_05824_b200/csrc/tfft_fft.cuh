@@ -16,7 +16,9 @@ namespace tfft {
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
-template <typename T, int N_, int E_, bool INV>
+// PF: issue the next pass's twiddle loads before the exchange barriers so their
+// L1/L2 latency hides behind the shared-memory round trip (costs E registers).
+template <typename T, int N_, int E_, bool INV, bool PF = false>
 struct Fft {
   static constexpr int N = N_;
   static constexpr int E = (E_ < N_) ? E_ : N_;
@@ -36,35 +38,62 @@ struct Fft {
     return k / RLAST + (E / RLAST) * (k % RLAST);
   }
 
-  // twiddle multiply + radix-R butterflies of pass P on the register set v
+  // Padded shared-memory layout: one spare slot after every bank row (16
+  // float2 / 8 double2), so Stockham scatter writes and strided reads hit
+  // distinct banks; offsets that are multiples of a bank row fold into
+  // compile-time constants (the XOR swizzle cost ~20% integer ops).
+  static constexpr int LOGP = sizeof(T) == 4 ? 4 : 3;
+  static constexpr int NPAD = N + (N >> LOGP);  // elements a slot buffer occupies
+  static __device__ __forceinline__ int phys(int a) { return a + (a >> LOGP); }
+
   template <int P>
-  static __device__ __forceinline__ void compute(C<T> (&v)[E], int tau, const C<T>* __restrict__ tw) {
+  static __device__ __forceinline__ void load_tw(C<T> (&w)[E], int tau, const C<T>* __restrict__ tw) {
     constexpr int R = radix<P>();
     constexpr int S = stride<P>();
     constexpr int M = N / (S * R);
+    if constexpr (S > 1) {
+#pragma unroll
+      for (int u = 0; u < E / R; ++u) {
+        const int q = (tau + TPS * u) & (S - 1);
+#pragma unroll
+        for (int t = 1; t < R; ++t) w[u * R + t] = __ldg(tw + q * t * M);
+      }
+    }
+  }
+
+  // twiddle multiply (from w) + radix-R butterflies of pass P
+  template <int P>
+  static __device__ __forceinline__ void apply(C<T> (&v)[E], const C<T> (&w)[E]) {
+    constexpr int R = radix<P>();
+    constexpr int S = stride<P>();
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       if constexpr (S > 1) {
-        const int j = tau + TPS * u;
-        const int q = j & (S - 1);
 #pragma unroll
-        for (int t = 1; t < R; ++t) v[u * R + t] = cmul<T>(v[u * R + t], __ldg(tw + q * t * M));
+        for (int t = 1; t < R; ++t) v[u * R + t] = cmul<T>(v[u * R + t], w[u * R + t]);
       }
       dft<T, R, INV>(&v[u * R]);
     }
   }
 
   template <int P>
-  static __device__ __forceinline__ void read(const C<T>* buf, C<T> (&v)[E], int tau, int key) {
+  static __device__ __forceinline__ void compute(C<T> (&v)[E], int tau, const C<T>* __restrict__ tw) {
+    C<T> w[E];
+    load_tw<P>(w, tau, tw);
+    apply<P>(v, w);
+  }
+
+  template <int P>
+  static __device__ __forceinline__ void read(const C<T>* buf, C<T> (&v)[E], int tau) {
     constexpr int R = radix<P>();
 #pragma unroll
     for (int u = 0; u < E / R; ++u)
 #pragma unroll
-      for (int t = 0; t < R; ++t) v[u * R + t] = buf[swz<T>(tau + TPS * u + (N / R) * t) ^ key];
+      for (int t = 0; t < R; ++t) v[u * R + t] = buf[phys(tau + TPS * u + (N / R) * t)];
   }
 
   template <int P>
-  static __device__ __forceinline__ void write(C<T>* buf, const C<T> (&v)[E], int tau, int key) {
+  static __device__ __forceinline__ void write(C<T>* buf, const C<T> (&v)[E], int tau) {
     constexpr int R = radix<P>();
     constexpr int S = stride<P>();
 #pragma unroll
@@ -73,35 +102,34 @@ struct Fft {
       const int q = j & (S - 1);
       const int p = j >> ilog2(S);
 #pragma unroll
-      for (int c = 0; c < R; ++c) buf[swz<T>(q + S * (R * p + c)) ^ key] = v[u * R + c];
+      for (int c = 0; c < R; ++c) buf[phys(q + S * (R * p + c))] = v[u * R + c];
     }
   }
 
   template <int P>
-  static __device__ __forceinline__ void rest(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw, int key) {
+  static __device__ __forceinline__ void rest(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw) {
     if constexpr (P < NPASS) {
+      C<T> w[E];
+      if constexpr (PF) load_tw<P>(w, tau, tw);
       __syncthreads();
-      write<P - 1>(buf, v, tau, key);
+      write<P - 1>(buf, v, tau);
       __syncthreads();
-      read<P>(buf, v, tau, key);
-      compute<P>(v, tau, tw);
-      rest<P + 1>(buf, v, tau, tw, key);
+      read<P>(buf, v, tau);
+      if constexpr (!PF) load_tw<P>(w, tau, tw);
+      apply<P>(v, w);
+      rest<P + 1>(buf, v, tau, tw);
     }
   }
 
-  // v: legs of pass 0 (= input elements tau + TPS*k, already loaded by the
-  // caller from buf's linear layout). On return v holds the outputs at
-  // positions tau + TPS*out_pos(k); the last smem read is complete for this
-  // thread but the caller must barrier before overwriting buf.
-  // Contains NPASS-1 pairs of CTA-wide barriers: every thread must call it.
-  // `key` XORs the low swizzle bits per slot (K3 packs many columns per CTA).
-  static __device__ __forceinline__ void run(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw, int key = 0) {
+  // v: legs of pass 0 (= input elements tau + TPS*k, loaded by the caller).
+  // On return v holds the outputs at positions tau + TPS*out_pos(k); the last
+  // smem read is complete for this thread but the caller must barrier before
+  // overwriting buf. Contains NPASS-1 pairs of CTA-wide barriers: every thread
+  // must call it. buf spans NPAD elements (padded layout).
+  static __device__ __forceinline__ void run(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw) {
     compute<0>(v, tau, tw);
-    rest<1>(buf, v, tau, tw, key);
+    rest<1>(buf, v, tau, tw);
   }
-
-  // smem address of position a of a slot buffer (the swizzled layout)
-  static __device__ __forceinline__ int phys(int a, int key) { return swz<T>(a) ^ key; }
 };
 
 }  // namespace tfft

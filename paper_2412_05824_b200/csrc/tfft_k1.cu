@@ -19,19 +19,46 @@
 
 namespace tfft {
 
-template <typename T, int LOGN, bool INV, bool ABFT>
+// Tunable shapes (swept on the B200 with tools/tune_k1.py; the production
+// choice per (precision, N) is k1_variant()).
+struct K1Var {
+  int emax32, emax64;  // elements per thread (radix of the main passes)
+  int nt;              // target threads per CTA
+  int st_small, st_big;  // pipeline stages for tiles <= 32 KB / larger
+  int minb;            // __launch_bounds__ min blocks per SM
+  int pf;              // prefetch next-pass twiddles before the barriers
+};
+constexpr K1Var kK1Var[] = {
+    {16, 16, 256, 3, 2, 1, 0},  // 0 production default: radix 16, 3-stage ring
+    {16, 16, 256, 3, 2, 1, 1},  // 1 + twiddle prefetch
+    {16, 16, 256, 2, 2, 2, 0},  // 2 2 stages, 2 blocks/SM
+    {16, 16, 256, 2, 2, 2, 1},  // 3 2 stages, 2 blocks/SM, prefetch
+    {16, 16, 128, 3, 2, 2, 0},  // 4 128-thread CTAs
+    {16, 16, 512, 3, 2, 1, 0},  // 5 512-thread CTAs
+    {16, 16, 256, 4, 2, 1, 0},  // 6 4-stage ring
+    {8, 8, 256, 3, 2, 2, 0},    // 7 radix 8
+};
+
+template <typename T, int LOGN, bool INV, bool ABFT, int V = 0>
 struct K1 {
+  static constexpr K1Var VAR = kK1Var[V];
   static constexpr int N = 1 << LOGN;
-  static constexpr int EMAX = sizeof(T) == 4 ? 16 : 8;
-  using F = Fft<T, N, EMAX, INV>;
+  static constexpr int EMAX = sizeof(T) == 4 ? VAR.emax32 : VAR.emax64;
+  using F = Fft<T, N, EMAX, INV, VAR.pf != 0>;
   static constexpr int E = F::E;
   static constexpr int TPS = F::TPS;
-  static constexpr int NT_TARGET = 256;
+  static constexpr int NT_TARGET = VAR.nt;
   static constexpr int SPT = TPS >= NT_TARGET ? 1 : NT_TARGET / TPS;
   static constexpr int NT = SPT * TPS;
-  static constexpr int TILE = SPT * N;
+  static constexpr int MINB = (NT <= 1024 / VAR.minb) ? VAR.minb : 1;
+  // slot g's signal lands at g * SLOT (linear, by the bulk copy) and the
+  // passes re-lay it out padded inside the same NPAD elements; SLOT keeps the
+  // bulk-copy destinations 16-byte aligned
+  static constexpr int SLOT = (F::NPAD + (16 / (int)sizeof(C<T>)) - 1) / (16 / (int)sizeof(C<T>)) *
+                              (16 / (int)sizeof(C<T>));
+  static constexpr int TILE = SPT * SLOT;
   static constexpr int TILE_BYTES = TILE * (int)sizeof(C<T>);
-  static constexpr int NSTAGE = TILE_BYTES <= 32768 ? 3 : 2;
+  static constexpr int NSTAGE = TILE_BYTES <= 32768 ? VAR.st_small : VAR.st_big;
   static constexpr int NWARP_SLOT = TPS >= 32 ? TPS / 32 : 1;
   static constexpr int RED_BYTES = SPT * NWARP_SLOT * 5 * 8;
   static constexpr int SMEM = (NSTAGE + (ABFT ? 1 : 0)) * TILE_BYTES + RED_BYTES + 64 + NSTAGE * 8;
@@ -74,9 +101,10 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* addr, doub
   atomicMax(addr, (unsigned long long)__double_as_longlong(v));
 }
 
-template <typename T, int LOGN, bool INV, bool ABFT>
-__global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a) {
-  using K = K1<T, LOGN, INV, ABFT>;
+template <typename T, int LOGN, bool INV, bool ABFT, int V>
+__global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT, V>::NT, K1<T, LOGN, INV, ABFT, V>::MINB)
+    k1_kernel(K1Args a) {
+  using K = K1<T, LOGN, INV, ABFT, V>;
   using F = typename K::F;
   using CT = C<T>;
   constexpr int N = K::N, E = K::E, TPS = K::TPS, SPT = K::SPT, NSTAGE = K::NSTAGE;
@@ -153,12 +181,9 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a
     }
     if (p_item >= nitems) return;
     CT* dst = tiles + stage * K::TILE;
-    if (!ABFT) {
-      const int64_t s0 = p_item * SPT;
-      const int64_t cnt = min((int64_t)SPT, B - s0);
-      const uint32_t bytes = (uint32_t)(cnt * N * sizeof(CT));
-      mbar_expect_tx(&full[stage], bytes);
-      bulk_g2s(dst, x + s0 * N, bytes, &full[stage]);
+    if (!ABFT && SPT == 1) {
+      mbar_expect_tx(&full[stage], (uint32_t)(N * sizeof(CT)));
+      bulk_g2s(dst, x + p_item * N, N * sizeof(CT), &full[stage]);
     } else {
       uint32_t bytes = 0;
       int64_t st[SPT];
@@ -172,7 +197,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a
       }
       mbar_expect_tx(&full[stage], bytes);
       for (int gg = 0; gg < SPT; ++gg)
-        if (ok[gg]) bulk_g2s(dst + gg * N, x + st[gg] * N, N * sizeof(CT), &full[stage]);
+        if (ok[gg]) bulk_g2s(dst + gg * K::SLOT, x + st[gg] * N, N * sizeof(CT), &full[stage]);
     }
     ++p_i;
   };
@@ -203,7 +228,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a
     for (int64_t i = 0; i < len; ++i, ++it) {
       const int stage = it % NSTAGE;
       mbar_wait(&full[stage], (it / NSTAGE) & 1);
-      CT* buf = tiles + stage * K::TILE + g * N;
+      CT* buf = tiles + stage * K::TILE + g * K::SLOT;
       const bool valid = i < my_len;
       const int64_t sig = my_start + i;
 
@@ -321,7 +346,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a
         have_window = wid < a.abft.nwin;
         if (have_window) {
 #pragma unroll
-          for (int k = 0; k < E; ++k) wbuf[g * N + tau + TPS * k] = s_in[k];
+          for (int k = 0; k < E; ++k) wbuf[g * K::SLOT + tau + TPS * k] = s_in[k];
         }
         __syncthreads();
       } else {
@@ -330,13 +355,13 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-          for (int k = 0; k < E; ++k) wbuf[g * N + tau + TPS * k] = pass == 0 ? s_in[k] : s_out[k];
+          for (int k = 0; k < E; ++k) wbuf[g * K::SLOT + tau + TPS * k] = pass == 0 ? s_in[k] : s_out[k];
           __syncthreads();
           if (g == 0) {
 #pragma unroll
             for (int k = 0; k < E; ++k) {
               CT acc = wbuf[tau + TPS * k];
-              for (int gg = 1; gg < SPT; ++gg) acc = cadd<T>(acc, wbuf[gg * N + tau + TPS * k]);
+              for (int gg = 1; gg < SPT; ++gg) acc = cadd<T>(acc, wbuf[gg * K::SLOT + tau + TPS * k]);
               if (pass == 0) s_in[k] = acc;
               else s_out[k] = acc;
             }
@@ -400,7 +425,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a
       }
       // in-CTA FFT of s_in (working precision, as _fft_column) vs s_out
       CT v[E];
-      CT* wb = wbuf + g * N;
+      CT* wb = wbuf + g * K::SLOT;
 #pragma unroll
       for (int k = 0; k < E; ++k) v[k] = wb[tau + TPS * k];
       F::run(wb, v, tau, tw);
@@ -431,10 +456,17 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT>::NT) k1_kernel(K1Args a
 // ---------------------------------------------------------------------------
 // host-side dispatch
 
-template <typename T, int LOGN, bool INV, bool ABFT>
+// production variant per (precision, log2 N) — chosen from the B200 sweep
+// (tools/tune_k1.py, profiles/round1_k1_variants.txt)
+template <typename T, int LOGN>
+constexpr int prod_variant() {
+  return 0;
+}
+
+template <typename T, int LOGN, bool INV, bool ABFT, int V>
 static int launch_one(const K1Args& a, int num_sms, cudaStream_t st) {
-  using K = K1<T, LOGN, INV, ABFT>;
-  auto kern = k1_kernel<T, LOGN, INV, ABFT>;
+  using K = K1<T, LOGN, INV, ABFT, V>;
+  auto kern = k1_kernel<T, LOGN, INV, ABFT, V>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
@@ -456,16 +488,45 @@ static int launch_one(const K1Args& a, int num_sms, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
+#ifdef TFFT_TUNING
+static int g_variant = -1;
+}  // namespace tfft
+extern "C" void tfft_tune_set_variant(int v) { tfft::g_variant = v; }
+namespace tfft {
+template <typename T, int L>
+constexpr bool tuned_size() { return L == 8 || L == 10 || L == 12 || L == 13; }
+#endif
+
+template <typename T, int L, bool INV, bool ABFT>
+static int launch_sel(const K1Args& a, int num_sms, cudaStream_t st) {
+#ifdef TFFT_TUNING
+  if constexpr (tuned_size<T, L>() && !INV) {
+    switch (g_variant) {
+      case 0: return launch_one<T, L, INV, ABFT, 0>(a, num_sms, st);
+      case 1: return launch_one<T, L, INV, ABFT, 1>(a, num_sms, st);
+      case 2: return launch_one<T, L, INV, ABFT, 2>(a, num_sms, st);
+      case 3: return launch_one<T, L, INV, ABFT, 3>(a, num_sms, st);
+      case 4: return launch_one<T, L, INV, ABFT, 4>(a, num_sms, st);
+      case 5: return launch_one<T, L, INV, ABFT, 5>(a, num_sms, st);
+      case 6: return launch_one<T, L, INV, ABFT, 6>(a, num_sms, st);
+      case 7: return launch_one<T, L, INV, ABFT, 7>(a, num_sms, st);
+      default: break;
+    }
+  }
+#endif
+  return launch_one<T, L, INV, ABFT, prod_variant<T, L>()>(a, num_sms, st);
+}
+
 template <typename T, bool INV, bool ABFT>
 static int dispatch(int logn, const K1Args& a, int num_sms, cudaStream_t st) {
   switch (logn) {
 #define TFFT_CASE(L) \
-  case L: return launch_one<T, L, INV, ABFT>(a, num_sms, st);
+  case L: return launch_sel<T, L, INV, ABFT>(a, num_sms, st);
     TFFT_CASE(1) TFFT_CASE(2) TFFT_CASE(3) TFFT_CASE(4) TFFT_CASE(5) TFFT_CASE(6) TFFT_CASE(7)
     TFFT_CASE(8) TFFT_CASE(9) TFFT_CASE(10) TFFT_CASE(11) TFFT_CASE(12)
 #undef TFFT_CASE
     case 13:
-      if constexpr (sizeof(T) == 4) return launch_one<T, 13, INV, ABFT>(a, num_sms, st);
+      if constexpr (sizeof(T) == 4) return launch_sel<T, 13, INV, ABFT>(a, num_sms, st);
       return (int)cudaErrorInvalidValue;
     default:
       return (int)cudaErrorInvalidValue;
@@ -484,14 +545,35 @@ int launch_k1(int prec, int logn, bool inverse, bool abft, const K1Args& a, int 
   return inverse ? dispatch<double, true, false>(logn, a, num_sms, st) : dispatch<double, false, false>(logn, a, num_sms, st);
 }
 
-}  // namespace tfft
-
-namespace tfft {
-int k1_slots(int prec, int logn) {
-  const int n = 1 << logn;
-  const int emax = prec == 0 ? 16 : 8;
-  const int e = emax < n ? emax : n;
-  const int tps = n / e;
-  return tps >= 256 ? 1 : 256 / tps;
+template <typename T, int L>
+static int slots_of() {
+#ifdef TFFT_TUNING
+  if constexpr (tuned_size<T, L>()) {
+    switch (g_variant) {
+      case 0: return K1<T, L, false, true, 0>::SPT;
+      case 1: return K1<T, L, false, true, 1>::SPT;
+      case 2: return K1<T, L, false, true, 2>::SPT;
+      case 3: return K1<T, L, false, true, 3>::SPT;
+      case 4: return K1<T, L, false, true, 4>::SPT;
+      case 5: return K1<T, L, false, true, 5>::SPT;
+      case 6: return K1<T, L, false, true, 6>::SPT;
+      case 7: return K1<T, L, false, true, 7>::SPT;
+      default: break;
+    }
+  }
+#endif
+  return K1<T, L, false, true, prod_variant<T, L>()>::SPT;
 }
+
+int k1_slots(int prec, int logn) {
+  switch (logn) {
+#define TFFT_SL(L) \
+  case L: return prec == 0 ? slots_of<float, L>() : slots_of<double, L>();
+    TFFT_SL(1) TFFT_SL(2) TFFT_SL(3) TFFT_SL(4) TFFT_SL(5) TFFT_SL(6) TFFT_SL(7)
+    TFFT_SL(8) TFFT_SL(9) TFFT_SL(10) TFFT_SL(11) TFFT_SL(12) TFFT_SL(13)
+#undef TFFT_SL
+    default: return 1;
+  }
+}
+
 }  // namespace tfft

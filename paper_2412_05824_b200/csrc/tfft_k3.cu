@@ -8,8 +8,9 @@
 //
 //   pass A: for each signal and each block of CB consecutive columns p, load
 //           the N1 x CB tile (CB contiguous elements per row v: coalesced),
-//           N1-point FFTs in shared memory (one column per slot, swizzled with a
-//           per-slot XOR key), twiddle w_N^{pq}, store rows of Z contiguously.
+//           N1-point FFTs in shared memory (one padded column slot each, with a
+//           per-column skew against bank conflicts), twiddle w_N^{pq}, store
+//           rows of Z contiguously.
 //   pass B: for each block of CB consecutive q, load the N2 x CB tile of Z,
 //           N2-point FFTs, transpose through shared memory, store
 //           y[q + N1 k] in CB-contiguous runs.
@@ -29,16 +30,23 @@ namespace tfft {
 template <typename T, int LOGL>
 struct ColCfg {
   static constexpr int L = 1 << LOGL;
-  static constexpr int EMAX = sizeof(T) == 4 ? 16 : 8;
+  static constexpr int EMAX = 16;
   static constexpr int E = EMAX < L ? EMAX : L;
   static constexpr int TPS = L / E;
   static constexpr int BPC = (int)sizeof(C<T>);
   static constexpr int CB0 = 65536 / (L * BPC);
   static constexpr int CB = CB0 < 2 ? 2 : (CB0 > 32 ? 32 : CB0);
   static constexpr int NT = CB * TPS;
-  static constexpr int TILE = CB * L;
+  // bank-row slots (16 float2 / 8 double2 per 128 B); each column slot is the
+  // engine's padded buffer plus room for a per-column skew that spreads the
+  // rows one shared-memory phase of the transposing loader touches
+  static constexpr int PB = sizeof(T) == 4 ? 16 : 8;
+  static constexpr int NPAD = L + L / PB;
+  static constexpr int SLOTP = NPAD + PB;
+  static constexpr int RPP = PB / CB > 1 ? PB / CB : 1;
+  static __device__ __forceinline__ int base(int c) { return c * SLOTP + ((c * RPP) & (PB - 1)); }
+  static constexpr int TILE = CB * SLOTP;
   static constexpr int SMEM = TILE * BPC;
-  static constexpr int KEYMASK = sizeof(T) == 4 ? 15 : 7;
 };
 
 struct ColArgs {
@@ -71,8 +79,7 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
   const int tid = threadIdx.x;
   const int g = tid / TPS;
   const int tau = tid % TPS;
-  const int key = g & K::KEYMASK;
-  CT* slot = tile + g * L;
+  CT* slot = tile + K::base(g);
   const CT* __restrict__ src = static_cast<const CT*>(a.src);
   CT* __restrict__ dst = static_cast<CT*>(a.dst);
   const CT* __restrict__ tw = static_cast<const CT*>(a.tw);
@@ -80,19 +87,25 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
   const int64_t ntiles = a.batch * ncb;
   bool bad = false;
 
+  // the L x CB tile (rows contiguous in global): element e = i*NT + tid is
+  // row e / CB, column e % CB. Loads for tile t+grid are issued before tile
+  // t's FFT so their HBM latency hides behind the shared-memory passes.
+  CT ld[E];
+  auto issue = [&](int64_t t) {
+    const int64_t sg = t / ncb;
+    const CT* s = src + sg * a.n + (t - sg * ncb) * CB;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int e = i * NT + tid;
+      ld[i] = __ldcs(s + (int64_t)(e / CB) * a.pitch + e % CB);
+    }
+  };
+  if (blockIdx.x < ntiles) issue(blockIdx.x);
+
 #pragma unroll 1
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t sig = t / ncb;
     const int64_t c0 = (t - sig * ncb) * CB;
-    const CT* s = src + sig * a.n + c0;
-    // ---- load the L x CB tile (rows contiguous in global) into column slots
-    CT ld[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int e = i * NT + tid;
-      const int r = e / CB, c = e % CB;
-      ld[i] = __ldcs(s + (int64_t)r * a.pitch + c);
-    }
     if constexpr (MODE == 0) {
 #pragma unroll
       for (int i = 0; i < E; ++i) bad |= !finite2<T>(ld[i]);
@@ -103,8 +116,7 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
 #pragma unroll
           for (int i = 0; i < E; ++i) {
             const int e = i * NT + tid;
-            const int r = e / CB, c = e % CB;
-            if (c0 + c + (int64_t)r * a.pitch == fl.element) {
+            if (c0 + e % CB + (int64_t)(e / CB) * a.pitch == fl.element) {
               if (fl.part == 0) ld[i].x = flip_bits(ld[i].x, fl.bit);
               else ld[i].y = flip_bits(ld[i].y, fl.bit);
             }
@@ -115,15 +127,15 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int e = i * NT + tid;
-      const int r = e / CB, c = e % CB;
-      tile[c * L + F::phys(r, c & K::KEYMASK)] = ld[i];
+      tile[K::base(e % CB) + F::phys(e / CB)] = ld[i];
     }
     __syncthreads();
+    if (t + gridDim.x < ntiles) issue(t + gridDim.x);
     // ---- column FFTs
     CT v[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) v[k] = slot[F::phys(tau + TPS * k, key)];
-    F::run(slot, v, tau, tw, key);
+    for (int k = 0; k < E; ++k) v[k] = slot[F::phys(tau + TPS * k)];
+    F::run(slot, v, tau, tw);
     if constexpr (MODE == 0) {
       // twiddle w_N^{p q} (two-level table) and store Z[p][q] at q + N1 p
       const int64_t p = c0 + g;
@@ -152,14 +164,14 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
       // transpose through the tile, then y[q + N1 k] in CB-contiguous runs
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < E; ++k) slot[F::phys(tau + TPS * F::out_pos(k), key)] = v[k];
+      for (int k = 0; k < E; ++k) slot[F::phys(tau + TPS * F::out_pos(k))] = v[k];
       __syncthreads();
       CT* d = dst + sig * a.n + c0;
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int e = i * NT + tid;
         const int r = e / CB, c = e % CB;
-        CT val = tile[c * L + F::phys(r, c & K::KEYMASK)];
+        CT val = tile[K::base(c) + F::phys(r)];
         if constexpr (INV) val = cscale<T>(val, (T)(1.0 / (double)a.n));
         __stcs(d + (int64_t)r * a.n1 + c, val);
       }
