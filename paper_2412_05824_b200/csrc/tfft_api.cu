@@ -328,7 +328,7 @@ int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, 
   if (p->mode == 1) {
     int rc = k3_execute(p->k3, x, y, batch, inverse, (const DevFault*)p->faults.p, (int)dev.size(),
                         (Counters*)counters, nullptr, st);
-    g_launches.fetch_add(2, std::memory_order_relaxed);
+    g_launches.fetch_add(k3_launches(p->k3), std::memory_order_relaxed);
     return rc ? cuda_fail(rc, "k3 launch") : 0;
   }
   return multipass(p, x, y, batch, inverse, st);

@@ -16,9 +16,20 @@ namespace tfft {
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
+// CTA-wide barrier (BAR_THREADS == 0) or a named barrier (id 1) over the
+// first BAR_THREADS threads, for warp-specialised kernels whose producer warp
+// does not take part in the exchanges.
+template <int BAR_THREADS>
+__device__ __forceinline__ void fft_sync() {
+  if constexpr (BAR_THREADS == 0) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"n"(BAR_THREADS) : "memory");
+}
+
 // PF: issue the next pass's twiddle loads before the exchange barriers so their
 // L1/L2 latency hides behind the shared-memory round trip (costs E registers).
-template <typename T, int N_, int E_, bool INV, bool PF = false>
+// TWS: the twiddle table pointer is a shared-memory copy (plain loads)
+// instead of a global table read through the read-only path.
+template <typename T, int N_, int E_, bool INV, bool PF = false, int BAR_THREADS = 0, bool TWS = false>
 struct Fft {
   static constexpr int N = N_;
   static constexpr int E = (E_ < N_) ? E_ : N_;
@@ -38,11 +49,12 @@ struct Fft {
     return k / RLAST + (E / RLAST) * (k % RLAST);
   }
 
-  // Padded shared-memory layout: one spare slot after every bank row (16
-  // float2 / 8 double2), so Stockham scatter writes and strided reads hit
-  // distinct banks; offsets that are multiples of a bank row fold into
-  // compile-time constants (the XOR swizzle cost ~20% integer ops).
-  static constexpr int LOGP = sizeof(T) == 4 ? 4 : 3;
+  // Padded shared-memory layout: one spare slot after every 16 elements, so
+  // Stockham scatter writes (consecutive threads 16 + 1 elements apart after a
+  // radix-16 pass) and strided reads hit distinct banks for both 8-byte and
+  // 16-byte elements; offsets that are multiples of 16 fold into compile-time
+  // constants (the XOR swizzle cost ~20% integer ops).
+  static constexpr int LOGP = 4;
   static constexpr int NPAD = N + (N >> LOGP);  // elements a slot buffer occupies
   static __device__ __forceinline__ int phys(int a) { return a + (a >> LOGP); }
 
@@ -56,7 +68,10 @@ struct Fft {
       for (int u = 0; u < E / R; ++u) {
         const int q = (tau + TPS * u) & (S - 1);
 #pragma unroll
-        for (int t = 1; t < R; ++t) w[u * R + t] = __ldg(tw + q * t * M);
+        for (int t = 1; t < R; ++t) {
+          if constexpr (TWS) w[u * R + t] = tw[q * t * M];
+          else w[u * R + t] = __ldg(tw + q * t * M);
+        }
       }
     }
   }
@@ -111,9 +126,9 @@ struct Fft {
     if constexpr (P < NPASS) {
       C<T> w[E];
       if constexpr (PF) load_tw<P>(w, tau, tw);
-      __syncthreads();
+      fft_sync<BAR_THREADS>();
       write<P - 1>(buf, v, tau);
-      __syncthreads();
+      fft_sync<BAR_THREADS>();
       read<P>(buf, v, tau);
       if constexpr (!PF) load_tw<P>(w, tau, tw);
       apply<P>(v, w);

@@ -23,6 +23,8 @@
 #include "tfft_fft.cuh"
 #include "tfft_internal.h"
 #include "tfft_k3.h"
+#include "tfft_k4.h"
+#include <cstdlib>
 #include "tfft_aux.h"
 
 namespace tfft {
@@ -243,6 +245,11 @@ struct K3Plan {
   void* enc[2] = {nullptr, nullptr};
   void* inter = nullptr;
   size_t inter_cap = 0;
+  bool k4 = false;       // fused L2-ring kernel available for this split
+  void* ring = nullptr;  // K4 intermediate ring (3 group slots)
+  size_t ring_cap = 0;
+  void* sync = nullptr;  // K4 ticket + per-group completion counters
+  size_t sync_cap = 0;
 };
 
 namespace {
@@ -307,6 +314,7 @@ int k3_create(int64_t n, int prec, const int64_t* spans, int nstages, int num_sm
   p->stage1 = nstages == 2;
   p->num_sms = num_sms;
   p->lo_bits = (logn + 1) / 2;
+  p->k4 = k4_supported(prec, l1, l2) && std::getenv("TFFT_NO_K4") == nullptr;
   const int64_t N1 = int64_t(1) << l1, N2 = int64_t(1) << l2;
   int e = 0;
   for (int c = 0; c < 2 && !e; ++c) {
@@ -333,14 +341,84 @@ void k3_destroy(K3Plan* p) {
     cudaFree(p->enc[c]);
   }
   cudaFree(p->inter);
+  cudaFree(p->ring);
+  cudaFree(p->sync);
   delete p;
 }
 
 bool k3_strikes_stage1(const K3Plan* p) { return p && p->stage1; }
 
+int k3_launches(const K3Plan* p) { return p && p->k4 ? 1 : 2; }
+
+// K4 group size: ~16 MB of intermediate per group, so the 3-slot ring is ~48 MB
+static int64_t k4_group(const K3Plan* p, int64_t batch) {
+  const int64_t cb = p->prec == 0 ? 8 : 16;
+  int64_t g = (int64_t(16) << 20) / (p->n * cb);
+  if (g < 1) g = 1;
+  if (g > batch) g = batch;
+  return g;
+}
+
+static int k4_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults,
+                      int nfaults, Counters* counters, cudaStream_t st) {
+  const size_t cb = p->prec == 0 ? 8 : 16;
+  const int64_t G = k4_group(p, batch);
+  const size_t ring = (size_t)3 * G * p->n * cb;
+  if (p->ring_cap < ring) {
+    cudaFree(p->ring);
+    p->ring = nullptr;
+    p->ring_cap = 0;
+    cudaError_t e = cudaMalloc(&p->ring, ring);
+    if (e != cudaSuccess) return (int)e;
+    p->ring_cap = ring;
+  }
+  const int64_t ng = (batch + G - 1) / G;
+  const size_t sync = 8 + (size_t)2 * ng * sizeof(unsigned);
+  if (p->sync_cap < sync) {
+    cudaFree(p->sync);
+    p->sync = nullptr;
+    p->sync_cap = 0;
+    cudaError_t e = cudaMalloc(&p->sync, sync);
+    if (e != cudaSuccess) return (int)e;
+    p->sync_cap = sync;
+  }
+  cudaError_t e = cudaMemsetAsync(p->sync, 0, sync, st);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t N1 = int64_t(1) << p->l1, N2 = int64_t(1) << p->l2;
+  const int64_t tpa = N2 / k4_columns_per_tile(p->prec, p->l1);  // pass-A tiles per signal
+  const int64_t tpb = N1 / k4_columns_per_tile(p->prec, p->l2);
+  const int64_t glast = batch - (ng - 1) * G;
+  const int c = inverse ? 1 : 0;
+  K4Args a{};
+  a.x = x;
+  a.y = y;
+  a.z = p->ring;
+  a.batch = batch;
+  a.group = G;
+  a.ngroups = ng;
+  a.ta = G * tpa;
+  a.tb = G * tpb;
+  a.ta_last = glast * tpa;
+  a.tb_last = glast * tpb;
+  a.tw1 = p->tw1[c];
+  a.tw2 = p->tw2[c];
+  a.hi = p->hi[c];
+  a.lo = p->lo[c];
+  a.lo_bits = p->lo_bits;
+  a.faults = faults;
+  a.nfaults = nfaults;
+  a.strike_stage = p->stage1 ? 1 : -1;
+  a.counters = counters;
+  a.ticket = static_cast<unsigned long long*>(p->sync);
+  a.done_a = reinterpret_cast<unsigned*>(static_cast<char*>(p->sync) + 8);
+  a.done_b = a.done_a + ng;
+  return launch_k4(p->prec, inverse != 0, p->l1, p->l2, a, p->num_sms, st);
+}
+
 int k3_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults, int nfaults,
                Counters* counters, void* reserved, cudaStream_t st) {
   (void)reserved;
+  if (p->k4) return k4_execute(p, x, y, batch, inverse, faults, nfaults, counters, st);
   const size_t cb = p->prec == 0 ? 8 : 16;
   const size_t need = (size_t)batch * p->n * cb;
   if (p->inter_cap < need) {

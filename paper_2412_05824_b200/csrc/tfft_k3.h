@@ -22,6 +22,8 @@ int k3_base_table(K3Plan* p, int prec, int64_t s, int r, int inverse, void* dst,
 // true when the two-pass split equals the reference's first stage span, so
 // stage-1 strikes land in-kernel on the canonical intermediate
 bool k3_strikes_stage1(const K3Plan* p);
+// kernel launches one k3_execute makes (1 with the fused K4 schedule)
+int k3_launches(const K3Plan* p);
 // omega_N^k / conj tables (built lazily; only the Jou encoding reads them)
 const void* k3_enc_table(K3Plan* p);
 const void* k3_enc_table_inv(K3Plan* p);

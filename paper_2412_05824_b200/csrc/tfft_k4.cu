@@ -1,0 +1,443 @@
+// K4: fused two-pass batched FFT for 2^13 <= N <= 2^22 with the four-step
+// intermediate held in L2 (one HBM read of x, one HBM write of y).
+//
+// Same factorisation and tile code as K3 (tfft_k3.cu): N = N1 x N2, pass A =
+// N1-point column FFTs of x viewed as N1 rows of N2 (+ twiddle w_N^{pq}),
+// pass B = N2-point column FFTs of Z' (N2 rows of N1) stored transposed into
+// y[q + N1 k]. The difference is the schedule: K3 runs pass A over the whole
+// batch, then pass B (the 2 x batch intermediate makes a full HBM round trip);
+// K4 is ONE persistent launch that walks the batch in groups of G signals,
+// interleaving the two passes as A(0) A(1) B(0) A(2) B(1) ... so pass B of a
+// group reads its intermediate about one group after pass A wrote it. The
+// intermediate lives in a ring of three group-sized slots (3 x ~16 MB), which
+// the 126 MB L2 holds: the slot is overwritten while its lines are still
+// dirty in L2, so the intermediate never costs HBM bandwidth.
+//
+// Work distribution: a global ticket counter hands out tiles in that order.
+// B(g) tiles wait (acquire) on the count of finished A(g) tiles; A(g) tiles
+// wait on B(g-3) (ring slot reuse). A CTA never blocks while holding an
+// unfinished tile (the next tile's dependency is only *polled* before the
+// current tile is computed; if it is not ready the CTA finishes and releases
+// its current tile first), and tiles are only handed to running CTAs, so the
+// earliest unfinished tile always has its dependencies met: the schedule is
+// deadlock-free without any residency assumption.
+//
+// Per tile: E elements per thread are loaded straight into registers for the
+// NEXT tile while the current one is transformed (x: streaming loads; Z:
+// L2-only .cg loads, so the ring's reuse can never hit a stale L1 line). The
+// thread -> (column, lane) map is column-fastest, so those registers are
+// already the FFT engine's (tfft_fft.cuh) pass-0 legs and pass B's outputs
+// are stored straight from registers in CB-element runs: shared memory only
+// carries the radix exchanges inside each column FFT. Fault strikes (stage 0 at load, stage 1 on
+// the canonical pass-A intermediate) and the non-finite input flag behave
+// exactly as in K3.
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through the runtime: no -lcuda)
+
+#include "tfft_fft.cuh"
+#include "tfft_internal.h"
+#include "tfft_k4.h"
+
+namespace tfft {
+
+// cuTensorMapEncodeTiled through cudaGetDriverEntryPoint (resolved once)
+static int k4_encode_2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t dim0, uint64_t dim1,
+                        uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return (int)cudaErrorNotSupported;
+    fn = reinterpret_cast<Fn>(p);
+  }
+  const cuuint64_t dims[2] = {dim0, dim1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+template <typename T, int LOGL, int E_, int NT_, bool INV>
+struct K4Ph {
+  static constexpr int L = 1 << LOGL;
+  using F = Fft<T, L, E_, INV, false, NT_, true>;  // consumer-only exchange barriers, smem twiddles
+  static constexpr int E = F::E;
+  static constexpr int TPS = F::TPS;
+  static constexpr int NT = NT_;
+  static constexpr int CB = NT / TPS;  // columns per tile
+  static_assert(CB >= 1 && CB * TPS == NT, "tile shape");
+  static constexpr int PB = sizeof(T) == 4 ? 16 : 8;  // complex slots per 128 B bank row
+  static constexpr int SLOTP = F::NPAD + PB;
+  static constexpr int RPP = PB / CB > 1 ? PB / CB : 1;
+  static __device__ __forceinline__ int base(int c) { return c * SLOTP + ((c * RPP) & (PB - 1)); }
+  static constexpr int ELEMS = CB * SLOTP;
+  static constexpr int BOXR = L < 256 ? L : 256;  // TMA box rows (box dims are <= 256)
+  static constexpr int NBOX = L / BOXR;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 2-D TMA box load global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ticket -> (phase, group, tile-in-group) for the order A0 A1 B0 A2 B1 ... B(ng-1)
+struct K4Item {
+  int phase;  // 0 = A, 1 = B, -1 = none
+  int64_t g;
+  int64_t r;
+};
+
+__device__ __forceinline__ K4Item k4_decode(const K4Args& a, int64_t t) {
+  const int64_t ta = a.ta, tb = a.tb, ng = a.ngroups, taL = a.ta_last, tbL = a.tb_last;
+  if (ng == 1) {
+    if (t < taL) return {0, 0, t};
+    t -= taL;
+    if (t < tbL) return {1, 0, t};
+    return {-1, 0, 0};
+  }
+  if (t < ta) return {0, 0, t};
+  const int64_t u = t - ta;
+  const int64_t h = u / (ta + tb) + 1;
+  if (h <= ng - 2) {
+    const int64_t r = u - (h - 1) * (ta + tb);
+    if (r < ta) return {0, h, r};
+    return {1, h - 1, r - ta};
+  }
+  int64_t r = t - (ta + (ng - 2) * (ta + tb));
+  if (r < taL) return {0, ng - 1, r};
+  r -= taL;
+  if (r < tb) return {1, ng - 2, r};
+  r -= tb;
+  if (r < tbL) return {1, ng - 1, r};
+  return {-1, 0, 0};
+}
+
+__device__ __forceinline__ bool k4_ready(const K4Args& a, const K4Item& it) {
+  if (it.phase == 0) {
+    if (it.g < 3) return true;
+    return ld_acquire(a.done_b + (it.g - 3)) >= (unsigned)a.tb;
+  }
+  const unsigned need = (unsigned)(it.g == a.ngroups - 1 ? a.ta_last : a.ta);
+  return ld_acquire(a.done_a + it.g) >= need;
+}
+
+template <typename T, int L1, int L2, bool INV, int E, int NT, int S>
+struct K4Cfg {
+  using PA = K4Ph<T, L1, E, NT, INV>;
+  using PB = K4Ph<T, L2, E, NT, INV>;
+  static constexpr int TILE = NT * E;  // elements per tile (both passes)
+  static constexpr int SLOTS = PA::ELEMS > PB::ELEMS ? PA::ELEMS : PB::ELEMS;
+  static constexpr int BPC = (int)sizeof(C<T>);
+  static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));  // shared twiddle tables
+  static constexpr int SMEM = (SLOTS + S * TILE + TWE) * BPC + S * 16 + S * 8 + 128;
+};
+
+// Warp-specialised: NT consumer threads (column FFTs) + one producer warp
+// whose elected lane draws tickets, waits for the tile's dependencies and
+// lands it with 2-D TMA boxes into an S-deep staging ring ([row][column]
+// dense). Consumers never wait on scheduling, only on data.
+template <typename T, int L1, int L2, bool INV, int E, int NT, int S>
+__global__ void __launch_bounds__(NT + 32, 1)
+    k4_kernel(const __grid_constant__ CUtensorMap tmx, K4Args a) {
+  using K = K4Cfg<T, L1, L2, INV, E, NT, S>;
+  using PA = typename K::PA;
+  using PB = typename K::PB;
+  using CT = C<T>;
+  constexpr int N1 = 1 << L1, N2 = 1 << L2;
+  constexpr int64_t N = int64_t(N1) * N2;
+  constexpr int LO = (L1 + L2 + 1) / 2;  // two-level w_N table split (tfft_k3.cu k3_create)
+  static_assert(PA::E == E && PB::E == E, "E elements per thread in both passes");
+  constexpr int ncbA = N2 / PA::CB;  // A tiles per signal
+  constexpr int ncbB = N1 / PB::CB;  // B tiles per signal
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  CT* slots = reinterpret_cast<CT*>(smem);
+  CT* stage = slots + K::SLOTS;
+  CT* tws1 = stage + S * K::TILE;                      // omega_N1 table (shared copy)
+  CT* tws2 = L1 == L2 ? tws1 : tws1 + N1;              // omega_N2 table
+  uint64_t* full = reinterpret_cast<uint64_t*>(tws1 + K::TWE);
+  uint64_t* empty = full + S;
+  long long* tk = reinterpret_cast<long long*>(empty + S);
+
+  const int tid = threadIdx.x;
+  const int G = (int)a.group;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NT / 32);
+    }
+    fence_mbar_init();
+  }
+  {
+    const CT* g1 = static_cast<const CT*>(a.tw1);
+    const CT* g2 = static_cast<const CT*>(a.tw2);
+    for (int i = tid; i < N1; i += NT + 32) tws1[i] = g1[i];
+    if constexpr (L1 != L2)
+      for (int i = tid; i < N2; i += NT + 32) tws2[i] = g2[i];
+  }
+  __syncthreads();
+
+  if (tid >= NT) {
+    // ------------------------------------------------------------ producer
+    if (tid != NT) return;
+    // Tickets are drawn two tiles ahead. Pass-A tiles (x, from HBM) are
+    // prefetched into L2 as soon as they are drawn, so bytes in flight are
+    // not bounded by the staging ring; the TMA into shared memory then only
+    // waits for L2. The current tile's dependency is resolved while the
+    // stage is still busy, so a freed stage only waits for the copy itself.
+    auto prefetch = [&](const K4Item& q) {
+      if (q.phase != 0) return;  // pass-B tiles are already L2-resident (the ring)
+      const int r = (int)q.r;
+      const int sl = r / ncbA;
+      const int c0 = (r - sl * ncbA) * PA::CB;
+      const int row0 = (int)((q.g * G + sl) * N1);
+#pragma unroll 1
+      for (int b = 0; b < PA::NBOX; ++b)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tmx)),
+                     "r"(c0 * 2), "r"(row0 + b * PA::BOXR)
+                     : "memory");
+    };
+    long long t = (long long)atomicAdd(a.ticket, 1ull);
+    K4Item item = k4_decode(a, t);
+    prefetch(item);
+    long long t2 = (long long)atomicAdd(a.ticket, 1ull);
+    K4Item item2 = k4_decode(a, t2);
+    prefetch(item2);
+#pragma unroll 1
+    for (int it = 0;; ++it) {
+      const int s = it % S;
+      if (item.phase >= 0) {
+        while (!k4_ready(a, item)) __nanosleep(32);
+        // the tile (pass B: written by other CTAs' generic stores) is read
+        // by the async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+      if (item.phase < 0) {
+        tk[s] = -1;
+        mbar_arrive(&full[s]);
+        return;
+      }
+      tk[s] = t;
+      CT* dst = stage + s * K::TILE;
+      const int r = (int)item.r;
+      if (item.phase == 0) {
+        const int sl = r / ncbA;
+        const int c0 = (r - sl * ncbA) * PA::CB;
+        const int row0 = (int)((item.g * G + sl) * N1);
+        mbar_expect_tx(&full[s], K::TILE * K::BPC);
+#pragma unroll 1
+        for (int b = 0; b < PA::NBOX; ++b)
+          tma_load_2d(dst + b * PA::BOXR * PA::CB, &tmx, c0 * 2, row0 + b * PA::BOXR, &full[s]);
+      } else {
+        // the ring is column-blocked: pass-B tile (signal sl, block j) is one
+        // contiguous run of N2 * CB_B elements
+        const CT* src = static_cast<const CT*>(a.z) + ((item.g % 3) * G + (r / ncbB)) * N +
+                        (int64_t)(r % ncbB) * K::TILE;
+        mbar_expect_tx(&full[s], K::TILE * K::BPC);
+        bulk_g2s(dst, src, K::TILE * K::BPC, &full[s]);
+      }
+      t = t2;
+      item = item2;
+      if (item.phase >= 0) {
+        t2 = (long long)atomicAdd(a.ticket, 1ull);
+        item2 = k4_decode(a, t2);
+        prefetch(item2);
+      }
+    }
+  }
+
+  // -------------------------------------------------------------- consumers
+  // thread -> (column g, lane tau), column fastest: staging reads are
+  // consecutive words and pass-B stores leave in CB-element runs
+  const int gA = tid % PA::CB, tA = tid / PA::CB;
+  const int gB = tid % PB::CB, tB = tid / PB::CB;
+  CT* __restrict__ y = static_cast<CT*>(a.y);
+  CT* __restrict__ z = static_cast<CT*>(a.z);
+  bool bad = false;
+
+#pragma unroll 1
+  for (int it = 0;; ++it) {
+    const int s = it % S;
+    mbar_wait(&full[s], (it / S) & 1);
+    const long long t = tk[s];
+    if (t < 0) break;
+    const K4Item cur = k4_decode(a, t);
+    const CT* st = stage + s * K::TILE;
+    CT v[E];
+    const int r = (int)cur.r;
+    if (cur.phase == 0) {
+      using P = PA;
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = st[(tA + P::TPS * k) * P::CB + gA];
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+      const int sl = r / ncbA;
+      const int64_t sig = cur.g * G + sl;
+      const int p = (r - sl * ncbA) * P::CB + gA;
+#pragma unroll
+      for (int k = 0; k < E; ++k) bad |= !finite2<T>(v[k]);
+      if (a.nfaults > 0) {  // stage-0 strikes on the freshly loaded input (fault.py:99-107)
+        for (int f = 0; f < a.nfaults; ++f) {
+          const DevFault fl = a.faults[f];
+          if (fl.signal != sig || fl.stage != 0) continue;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (p + (int64_t)(tA + P::TPS * k) * N2 == fl.element) {
+              if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
+              else v[k].y = flip_bits(v[k].y, fl.bit);
+            }
+        }
+      }
+      // big four-step twiddle w_N^{p q}, q = tA + TPS j: base w_N^{p tA} times
+      // step^j with step = w_N^{p TPS}; the two table pairs are fetched now so
+      // their latency hides behind the column FFT
+      const CT* __restrict__ hi = static_cast<const CT*>(a.hi);
+      const CT* __restrict__ lo = static_cast<const CT*>(a.lo);
+      constexpr unsigned LOM = (1u << LO) - 1;
+      const unsigned mb = (unsigned)p * (unsigned)tA, ms = (unsigned)p * (unsigned)P::TPS;
+      const CT bh = __ldg(hi + (mb >> LO)), bl = __ldg(lo + (mb & LOM));
+      const CT sh = __ldg(hi + (ms >> LO)), sl_ = __ldg(lo + (ms & LOM));
+      P::F::run(slots + P::base(gA), v, tA, tws1);
+      // blocked ring layout: Z'[p][q] at ((q / CB_B) * N2 + p) * CB_B + q % CB_B
+      CT* d = z + ((cur.g % 3) * G + sl) * N + p * PB::CB;
+      const CT step = cmul<T>(sh, sl_);
+      CT w = cmul<T>(bh, bl);  // running w_N^{p (tA + TPS j)}, j ascending (<= E-1 products)
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        constexpr int RL = P::F::RLAST;
+        const int k = (j % (E / RL)) * RL + j / (E / RL);  // register holding output position j
+        const int q = tA + P::TPS * j;
+        if (a.nfaults > 0 && a.strike_stage == 1) {  // canonical stage-1 intermediate
+          for (int f = 0; f < a.nfaults; ++f) {
+            const DevFault fl = a.faults[f];
+            if (fl.signal == sig && fl.stage == 1 && fl.element == q + (int64_t)p * N1) {
+              if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
+              else v[k].y = flip_bits(v[k].y, fl.bit);
+            }
+          }
+        }
+        d[(q / PB::CB) * (N2 * PB::CB) + (q % PB::CB)] = cmul<T>(v[k], w);
+        if (j + 1 < E) w = cmul<T>(w, step);
+      }
+    } else {
+      using P = PB;
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = st[(tB + P::TPS * k) * P::CB + gB];
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+      {
+        // the tile's ring lines are dead now: drop them from L2 without a
+        // write-back (the slot is fully rewritten by pass A three groups on)
+        const char* src = reinterpret_cast<const char*>(z + ((cur.g % 3) * G + (r / ncbB)) * N +
+                                                        (int64_t)(r % ncbB) * K::TILE);
+#pragma unroll 1
+        for (int i = tid; i < K::TILE * K::BPC / 128; i += NT)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(src + (int64_t)i * 128) : "memory");
+      }
+      P::F::run(slots + P::base(gB), v, tB, tws2);
+      const int sl = r / ncbB;
+      const int q0 = (r - sl * ncbB) * P::CB;
+      CT* d = y + (cur.g * G + sl) * N + q0 + gB;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        CT val = v[k];
+        if constexpr (INV) val = cscale<T>(val, (T)(1.0 / (double)N));
+        __stcs(d + (int64_t)(tB + P::TPS * P::F::out_pos(k)) * N1, val);
+      }
+    }
+    fft_sync<NT>();  // every consumer's stores are issued (release below)
+    if (tid == 0) red_release_add(cur.phase == 0 ? a.done_a + cur.g : a.done_b + cur.g, 1u);
+  }
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
+}
+
+template <typename T, int L1, int L2, bool INV, int E, int NT, int S>
+static int launch_k4_t(const K4Args& a, int num_sms, cudaStream_t st) {
+  using K = K4Cfg<T, L1, L2, INV, E, NT, S>;
+  auto kern = k4_kernel<T, L1, L2, INV, E, NT, S>;
+  static bool configured = false;
+  static int per_sm = 1;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT + 32, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    if (per_sm < 1) per_sm = 1;
+    configured = true;
+  }
+  const int64_t total = (a.ngroups - 1) * (a.ta + a.tb) + a.ta_last + a.tb_last;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > total) grid = total;
+  if (grid < 1) return 0;
+  // tensor map: x as (B*N1) rows of N2 complex
+  CUtensorMap tmx;
+  const int bpc = (int)sizeof(C<T>);
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  int rc = k4_encode_2d(&tmx, dt, const_cast<void*>(a.x), (uint64_t)(2 << L2), (uint64_t)a.batch << L1,
+                        (uint64_t)bpc << L2, (uint32_t)(2 * K::PA::CB), (uint32_t)K::PA::BOXR);
+  if (rc) return rc;
+  kern<<<(unsigned)grid, NT + 32, K::SMEM, st>>>(tmx, a);
+  return (int)cudaGetLastError();
+}
+
+// production tile shapes: 16 elements x 256 consumer threads (4096-element
+// tiles: 64 KB FP64 with one staging buffer, 32 KB FP32 with two)
+template <typename T> struct K4Shape;
+template <> struct K4Shape<double> { static constexpr int E = 16, NT = 256, S = 1; };
+template <> struct K4Shape<float> { static constexpr int E = 16, NT = 256, S = 2; };
+
+template <typename T>
+int k4_tile_cols(int logl) {
+  return K4Shape<T>::NT / ((1 << logl) / K4Shape<T>::E);
+}
+
+int k4_columns_per_tile(int prec, int logl) { return prec == 0 ? k4_tile_cols<float>(logl) : k4_tile_cols<double>(logl); }
+
+template <typename T, bool INV>
+static int dispatch_k4(int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
+  constexpr int E = K4Shape<T>::E, NT = K4Shape<T>::NT, S = K4Shape<T>::S;
+#define TFFT_K4(A, B) \
+  if (l1 == A && l2 == B) return launch_k4_t<T, A, B, INV, E, NT, S>(a, num_sms, st);
+  TFFT_K4_PAIRS
+#undef TFFT_K4
+  return (int)cudaErrorInvalidValue;
+}
+
+bool k4_supported(int prec, int l1, int l2) {
+#define TFFT_K4(A, B) \
+  if (l1 == A && l2 == B) return true;
+  TFFT_K4_PAIRS
+#undef TFFT_K4
+  (void)prec;
+  return false;
+}
+
+int launch_k4(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
+  if (prec == 0)
+    return inverse ? dispatch_k4<float, true>(l1, l2, a, num_sms, st) : dispatch_k4<float, false>(l1, l2, a, num_sms, st);
+  return inverse ? dispatch_k4<double, true>(l1, l2, a, num_sms, st) : dispatch_k4<double, false>(l1, l2, a, num_sms, st);
+}
+
+}  // namespace tfft

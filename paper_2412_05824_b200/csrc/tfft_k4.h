@@ -1,0 +1,46 @@
+// K4: fused two-pass batched FFT with an L2-resident intermediate ring
+// (tfft_k4.cu). Library-private.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tfft_internal.h"
+
+namespace tfft {
+
+// (log2 N1, log2 N2) splits with a compiled K4 instantiation: the reference's
+// balanced two-stage splits for 2^13..2^22 (plan.py _stage_exponents) plus the
+// curated 2^17 row (256, 512)
+#define TFFT_K4_PAIRS \
+  TFFT_K4(7, 6) TFFT_K4(7, 7) TFFT_K4(8, 7) TFFT_K4(8, 8) TFFT_K4(8, 9) TFFT_K4(9, 9) TFFT_K4(10, 9) \
+  TFFT_K4(10, 10) TFFT_K4(11, 10) TFFT_K4(11, 11)
+
+struct K4Args {
+  const void* x;
+  void* y;
+  void* z;               // intermediate ring: 3 slots of group * N elements
+  int64_t batch;
+  int64_t group;         // G signals per group
+  int64_t ngroups;
+  int64_t ta, tb;        // pass-A / pass-B tiles of a full group
+  int64_t ta_last, tb_last;  // ... of the last group
+  const void* tw1;       // omega_N1^m (conj for inverse)
+  const void* tw2;       // omega_N2^m
+  const void* hi;        // omega_N^{h 2^lo_bits}
+  const void* lo;        // omega_N^l
+  int lo_bits;
+  const DevFault* faults;
+  int nfaults;
+  int strike_stage;      // 1 when pass A's output is the reference's stage-1 boundary, else -1
+  Counters* counters;
+  unsigned long long* ticket;  // zeroed before the launch
+  unsigned* done_a;      // [ngroups] finished pass-A tiles, zeroed before the launch
+  unsigned* done_b;      // [ngroups]
+};
+
+bool k4_supported(int prec, int l1, int l2);
+int k4_columns_per_tile(int prec, int logl);
+int launch_k4(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
+
+}  // namespace tfft

@@ -219,3 +219,27 @@ def test_multipass_beyond_two_pass(precision):
     assert rel_l2(y, ref) <= l2_tol(precision, n)
     back = tf.execute_plan(plan, tf.SignalBatch(y), "inverse").data
     assert max_rel_error(back, x) <= (1e-5 if precision == "single" else 1e-12)
+
+
+@pytest.mark.parametrize("precision,log2n,groups", [("single", 14, 5), ("double", 16, 6), ("single", 20, 7),
+                                                   ("double", 13, 4), ("double", 17, 5)])
+def test_fused_two_pass_many_groups(precision, log2n, groups):
+    """K4 (fused two-pass, L2 intermediate ring): batches spanning several
+    ring cycles plus a short last group, against numpy's FFT in FP64, and
+    bitwise equal to the same signals transformed alone (no cross-signal or
+    cross-group leakage through the ring)."""
+    tf = _tf()
+    n = 2 ** log2n
+    bpc = 8 if precision == "single" else 16
+    g = max(1, (16 << 20) // (n * bpc))  # K4 group size (tfft_k3.cu k4_group)
+    b = g * groups + max(1, g // 3)
+    x = gaussian(n, b, precision, seed=log2n + 100)
+    plan = tf.build_plan(tf.select_params(n, b, precision), precision)
+    y = tf.execute_plan(plan, tf.SignalBatch(x)).data
+    ref = np.fft.fft(x.astype(np.complex128), axis=1)
+    assert rel_l2(y, ref) <= l2_tol(precision, n)
+    for sel in (slice(0, 1), slice(b - 1, b), slice(g - 1, g + 1)):
+        part = tf.execute_plan(plan, tf.SignalBatch(np.ascontiguousarray(x[sel]))).data
+        assert np.array_equal(part, y[sel])
+    back = tf.execute_plan(plan, tf.SignalBatch(y), "inverse").data
+    assert max_rel_error(back, x) <= (1e-5 if precision == "single" else 1e-12)
