@@ -80,9 +80,15 @@ struct K4Ph {
   static constexpr int NBOX = L / BOXR;
 };
 
+// Dependency counters are polled with relaxed L2 loads: an acquire would
+// invalidate the SM's whole L1 (CCTL.IVALL) on every poll, evicting the
+// twiddle tables of both resident CTAs. The data the counter guards is only
+// ever read by the TMA engine (async proxy, straight from L2) after a
+// fence.proxy.async, and the writer's release (MEMBAR.GPU before the count)
+// has made it globally performed, so no L1 copy can be stale.
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
@@ -149,15 +155,16 @@ struct K4Cfg {
   static constexpr int SLOTS = PA::ELEMS > PB::ELEMS ? PA::ELEMS : PB::ELEMS;
   static constexpr int BPC = (int)sizeof(C<T>);
   static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));  // shared twiddle tables
-  static constexpr int SMEM = (SLOTS + S * TILE + TWE) * BPC + S * 16 + S * 8 + 128;
+  static constexpr int RR = 4;  // release ring depth (consumer -> releaser warp)
+  static constexpr int SMEM = (SLOTS + S * TILE + TWE) * BPC + S * 16 + S * 8 + RR * 24 + 128;
 };
 
 // Warp-specialised: NT consumer threads (column FFTs) + one producer warp
 // whose elected lane draws tickets, waits for the tile's dependencies and
 // lands it with 2-D TMA boxes into an S-deep staging ring ([row][column]
 // dense). Consumers never wait on scheduling, only on data.
-template <typename T, int L1, int L2, bool INV, int E, int NT, int S>
-__global__ void __launch_bounds__(NT + 32, 1)
+template <typename T, int L1, int L2, bool INV, int E, int NT, int S, int MINB>
+__global__ void __launch_bounds__(NT + 64, MINB)
     k4_kernel(const __grid_constant__ CUtensorMap tmx, K4Args a) {
   using K = K4Cfg<T, L1, L2, INV, E, NT, S>;
   using PA = typename K::PA;
@@ -177,7 +184,10 @@ __global__ void __launch_bounds__(NT + 32, 1)
   CT* tws2 = L1 == L2 ? tws1 : tws1 + N1;              // omega_N2 table
   uint64_t* full = reinterpret_cast<uint64_t*>(tws1 + K::TWE);
   uint64_t* empty = full + S;
-  long long* tk = reinterpret_cast<long long*>(empty + S);
+  uint64_t* done = empty + S;          // [RR] consumer warps finished a tile's stores
+  uint64_t* relfree = done + K::RR;    // [RR] releaser consumed the ring entry
+  long long* tk = reinterpret_cast<long long*>(relfree + K::RR);
+  long long* rtk = tk + S;             // [RR] ticket of each finished tile
 
   const int tid = threadIdx.x;
   const int G = (int)a.group;
@@ -186,17 +196,40 @@ __global__ void __launch_bounds__(NT + 32, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NT / 32);
     }
+    for (int i = 0; i < K::RR; ++i) {
+      mbar_init(&done[i], NT / 32);
+      mbar_init(&relfree[i], 1);
+    }
     fence_mbar_init();
   }
   {
     const CT* g1 = static_cast<const CT*>(a.tw1);
     const CT* g2 = static_cast<const CT*>(a.tw2);
-    for (int i = tid; i < N1; i += NT + 32) tws1[i] = g1[i];
+    for (int i = tid; i < N1; i += NT + 64) tws1[i] = g1[i];
     if constexpr (L1 != L2)
-      for (int i = tid; i < N2; i += NT + 32) tws2[i] = g2[i];
+      for (int i = tid; i < N2; i += NT + 64) tws2[i] = g2[i];
   }
   __syncthreads();
 
+  if (tid >= NT + 32) {
+    // ------------------------------------------------------------ releaser
+    // Publishes finished tiles to the other CTAs: after all consumer warps
+    // arrived on done[], one gpu-scope fence orders every consumer's stores
+    // (cumulatively, through the mbarrier's CTA-scope release/acquire) before
+    // the completion count. The fence latency is paid here, off the
+    // consumers' critical path.
+    if (tid != NT + 32) return;
+#pragma unroll 1
+    for (int it = 0;; ++it) {
+      const int i = it % K::RR;
+      mbar_wait(&done[i], (it / K::RR) & 1);
+      const long long t = rtk[i];
+      if (t < 0) return;
+      const K4Item c = k4_decode(a, t);
+      red_release_add(c.phase == 0 ? a.done_a + c.g : a.done_b + c.g, 1u);
+      mbar_arrive(&relfree[i]);
+    }
+  }
   if (tid >= NT) {
     // ------------------------------------------------------------ producer
     if (tid != NT) return;
@@ -282,7 +315,14 @@ __global__ void __launch_bounds__(NT + 32, 1)
     const int s = it % S;
     mbar_wait(&full[s], (it / S) & 1);
     const long long t = tk[s];
-    if (t < 0) break;
+    const int ri = it % K::RR;
+    if (it >= K::RR) mbar_wait(&relfree[ri], ((it / K::RR) & 1) ^ 1);
+    if (tid == 0) rtk[ri] = t;
+    if (t < 0) {
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&done[ri]);
+      break;
+    }
     const K4Item cur = k4_decode(a, t);
     const CT* st = stage + s * K::TILE;
     CT v[E];
@@ -367,22 +407,22 @@ __global__ void __launch_bounds__(NT + 32, 1)
         __stcs(d + (int64_t)(tB + P::TPS * P::F::out_pos(k)) * N1, val);
       }
     }
-    fft_sync<NT>();  // every consumer's stores are issued (release below)
-    if (tid == 0) red_release_add(cur.phase == 0 ? a.done_a + cur.g : a.done_b + cur.g, 1u);
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&done[ri]);  // this warp's stores are issued
   }
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
 }
 
-template <typename T, int L1, int L2, bool INV, int E, int NT, int S>
+template <typename T, int L1, int L2, bool INV, int E, int NT, int S, int MINB>
 static int launch_k4_t(const K4Args& a, int num_sms, cudaStream_t st) {
   using K = K4Cfg<T, L1, L2, INV, E, NT, S>;
-  auto kern = k4_kernel<T, L1, L2, INV, E, NT, S>;
+  auto kern = k4_kernel<T, L1, L2, INV, E, NT, S, MINB>;
   static bool configured = false;
   static int per_sm = 1;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT + 32, K::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT + 64, K::SMEM);
     if (e != cudaSuccess) return (int)e;
     if (per_sm < 1) per_sm = 1;
     configured = true;
@@ -398,15 +438,16 @@ static int launch_k4_t(const K4Args& a, int num_sms, cudaStream_t st) {
   int rc = k4_encode_2d(&tmx, dt, const_cast<void*>(a.x), (uint64_t)(2 << L2), (uint64_t)a.batch << L1,
                         (uint64_t)bpc << L2, (uint32_t)(2 * K::PA::CB), (uint32_t)K::PA::BOXR);
   if (rc) return rc;
-  kern<<<(unsigned)grid, NT + 32, K::SMEM, st>>>(tmx, a);
+  kern<<<(unsigned)grid, NT + 64, K::SMEM, st>>>(tmx, a);
   return (int)cudaGetLastError();
 }
 
-// production tile shapes: 16 elements x 256 consumer threads (4096-element
-// tiles: 64 KB FP64 with one staging buffer, 32 KB FP32 with two)
+// production tile shapes: 16 elements x 128 consumer threads (2048-element
+// tiles) and two CTAs per SM, so one CTA's exchange barriers overlap the
+// other's radix arithmetic
 template <typename T> struct K4Shape;
-template <> struct K4Shape<double> { static constexpr int E = 16, NT = 256, S = 1; };
-template <> struct K4Shape<float> { static constexpr int E = 16, NT = 256, S = 2; };
+template <> struct K4Shape<double> { static constexpr int E = 16, NT = 128, S = 1, MINB = 2; };
+template <> struct K4Shape<float> { static constexpr int E = 16, NT = 256, S = 2, MINB = 1; };
 
 template <typename T>
 int k4_tile_cols(int logl) {
@@ -417,21 +458,29 @@ int k4_columns_per_tile(int prec, int logl) { return prec == 0 ? k4_tile_cols<fl
 
 template <typename T, bool INV>
 static int dispatch_k4(int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
-  constexpr int E = K4Shape<T>::E, NT = K4Shape<T>::NT, S = K4Shape<T>::S;
+  constexpr int E = K4Shape<T>::E, NT = K4Shape<T>::NT, S = K4Shape<T>::S, MINB = K4Shape<T>::MINB;
 #define TFFT_K4(A, B) \
-  if (l1 == A && l2 == B) return launch_k4_t<T, A, B, INV, E, NT, S>(a, num_sms, st);
+  if (l1 == A && l2 == B) return launch_k4_t<T, A, B, INV, E, NT, S, MINB>(a, num_sms, st);
   TFFT_K4_PAIRS
 #undef TFFT_K4
   return (int)cudaErrorInvalidValue;
 }
 
+// a split runs on K4 when it is instantiated and both passes' TMA rows are at
+// least 16 bytes (CB columns of complex values)
+template <typename T>
+static bool k4_shape_ok(int l1, int l2) {
+  return 2 * k4_tile_cols<T>(l1) * (int)sizeof(T) >= 16 && 2 * k4_tile_cols<T>(l2) * (int)sizeof(T) >= 16;
+}
+
 bool k4_supported(int prec, int l1, int l2) {
+  bool inst = false;
 #define TFFT_K4(A, B) \
-  if (l1 == A && l2 == B) return true;
+  if (l1 == A && l2 == B) inst = true;
   TFFT_K4_PAIRS
 #undef TFFT_K4
-  (void)prec;
-  return false;
+  if (!inst) return false;
+  return prec == 0 ? k4_shape_ok<float>(l1, l2) : k4_shape_ok<double>(l1, l2);
 }
 
 int launch_k4(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
