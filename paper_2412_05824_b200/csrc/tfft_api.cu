@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <algorithm>
 #include <atomic>
 #include <string>
@@ -119,6 +120,7 @@ struct tfft_plan {
   int num_sms = 148;
   int device = 0;
   bool k1 = false;
+  bool k5 = false;  // plain single-pass transforms run on the warp-specialised K5
   int mode = 0;              // 0: K1 single pass, 1: K3 two pass, 2: reference-order multipass
   DevBuf tw_fwd, tw_inv;     // omega_N^k, conj (K1 and ABFT encodings)
   DevBuf enc_tab[2];         // omega_N^k / conj for K3/multipass Jou encoding (lazy)
@@ -322,7 +324,10 @@ int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, 
     a.faults = (const DevFault*)p->faults.p;
     a.nfaults = (int)dev.size();
     a.counters = (Counters*)counters;
-    TFFT_TRY(launch_k1(p->prec, p->logn, inverse != 0, false, a, p->num_sms, st), "k1 launch");
+    if (p->k5)
+      TFFT_TRY(launch_k5(p->prec, p->logn, inverse != 0, a, p->num_sms, st), "k5 launch");
+    else
+      TFFT_TRY(launch_k1(p->prec, p->logn, inverse != 0, false, a, p->num_sms, st), "k1 launch");
     return 0;
   }
   if (p->mode == 1) {
@@ -368,6 +373,9 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
   cudaGetDevice(&p->device);
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device);
   p->k1 = k1_supported(precision, p->logn) != 0;
+  // K5 measured faster than K1 from N = 512 up; K1's wide 256-thread CTAs
+  // (16 signals per tile) still win at N <= 256 (profiles/r1s2_k5)
+  p->k5 = p->k1 && p->logn >= 9 && std::getenv("TFFT_NO_K5") == nullptr;
   if (p->k1) {
     std::vector<long double> re, im;
     fill_twiddles(re, im, n);

@@ -27,8 +27,12 @@ __device__ __forceinline__ void fft_sync() {
 
 // PF: issue the next pass's twiddle loads before the exchange barriers so their
 // L1/L2 latency hides behind the shared-memory round trip (costs E registers).
-// TWS: the twiddle table pointer is a shared-memory copy (plain loads)
-// instead of a global table read through the read-only path.
+// TWS: where the twiddles come from.
+//   false: the global w_N table (tw[m] = w_N^m), read through the read-only path;
+//   true : per-pass tables in shared memory built by build_pass_tables():
+//          pass P's block holds w_{S R}^{q t} at (t - 1) * S + q, q fastest, so
+//          the lanes of a warp (consecutive q) read consecutive words: no bank
+//          conflicts, unlike strided reads of a w_N copy (up to 8-way).
 template <typename T, int N_, int E_, bool INV, bool PF = false, int BAR_THREADS = 0, bool TWS = false>
 struct Fft {
   static constexpr int N = N_;
@@ -58,6 +62,35 @@ struct Fft {
   static constexpr int NPAD = N + (N >> LOGP);  // elements a slot buffer occupies
   static __device__ __forceinline__ int phys(int a) { return a + (a >> LOGP); }
 
+  // offset of pass P's block in the per-pass table: sum over earlier passes
+  // P' >= 1 of (R' - 1) S' (= S_P - E for P >= 1); PASS_TABLE entries in all
+  template <int P>
+  __host__ __device__ static constexpr int pass_off() {
+    if constexpr (P <= 1) return 0;
+    else return pass_off<P - 1>() + (radix<P - 1>() - 1) * stride<P - 1>();
+  }
+  static constexpr int PASS_TABLE = NPASS > 1 ? N - E : 0;
+
+  // per-pass twiddle tables from the global w_N table (direction included),
+  // cooperatively by threads [tid0, tid0 + nthr)
+  static __device__ __forceinline__ void build_pass_tables(C<T>* dst, const C<T>* __restrict__ wn, int tid,
+                                                           int nthr) {
+    build_from<1>(dst, wn, tid, nthr);
+  }
+  template <int P>
+  static __device__ __forceinline__ void build_from(C<T>* dst, const C<T>* __restrict__ wn, int tid, int nthr) {
+    if constexpr (P < NPASS) {
+      constexpr int R = radix<P>();
+      constexpr int S = stride<P>();
+      constexpr int M = N / (S * R);
+      for (int i = tid; i < (R - 1) * S; i += nthr) {
+        const int t = i / S + 1, q = i % S;
+        dst[pass_off<P>() + i] = wn[q * t * M];
+      }
+      build_from<P + 1>(dst, wn, tid, nthr);
+    }
+  }
+
   template <int P>
   static __device__ __forceinline__ void load_tw(C<T> (&w)[E], int tau, const C<T>* __restrict__ tw) {
     constexpr int R = radix<P>();
@@ -69,7 +102,7 @@ struct Fft {
         const int q = (tau + TPS * u) & (S - 1);
 #pragma unroll
         for (int t = 1; t < R; ++t) {
-          if constexpr (TWS) w[u * R + t] = tw[q * t * M];
+          if constexpr (TWS) w[u * R + t] = tw[pass_off<P>() + (t - 1) * S + q];
           else w[u * R + t] = __ldg(tw + q * t * M);
         }
       }

@@ -60,6 +60,8 @@ struct K1Args {
 // launchers (return cudaError_t as int)
 int launch_k1(int prec, int logn, bool inverse, bool abft, const K1Args& a, int num_sms, cudaStream_t st);
 int k1_supported(int prec, int logn);
+// K5: warp-specialised single-pass kernel (same sizes and results as K1's plain path)
+int launch_k5(int prec, int logn, bool inverse, const K1Args& a, int num_sms, cudaStream_t st);
 
 }  // namespace tfft
 

@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(NT + 64, MINB)
   extern __shared__ __align__(128) unsigned char smem[];
   CT* slots = reinterpret_cast<CT*>(smem);
   CT* stage = slots + K::SLOTS;
-  CT* tws1 = stage + S * K::TILE;                      // omega_N1 table (shared copy)
-  CT* tws2 = L1 == L2 ? tws1 : tws1 + N1;              // omega_N2 table
+  CT* tws1 = stage + S * K::TILE;                      // pass A per-pass twiddle tables
+  CT* tws2 = L1 == L2 ? tws1 : tws1 + N1;              // pass B's
   uint64_t* full = reinterpret_cast<uint64_t*>(tws1 + K::TWE);
   uint64_t* empty = full + S;
   uint64_t* done = empty + S;          // [RR] consumer warps finished a tile's stores
@@ -202,13 +202,8 @@ __global__ void __launch_bounds__(NT + 64, MINB)
     }
     fence_mbar_init();
   }
-  {
-    const CT* g1 = static_cast<const CT*>(a.tw1);
-    const CT* g2 = static_cast<const CT*>(a.tw2);
-    for (int i = tid; i < N1; i += NT + 64) tws1[i] = g1[i];
-    if constexpr (L1 != L2)
-      for (int i = tid; i < N2; i += NT + 64) tws2[i] = g2[i];
-  }
+  PA::F::build_pass_tables(tws1, static_cast<const CT*>(a.tw1), tid, NT + 64);
+  if constexpr (L1 != L2) PB::F::build_pass_tables(tws2, static_cast<const CT*>(a.tw2), tid, NT + 64);
   __syncthreads();
 
   if (tid >= NT + 32) {
