@@ -473,7 +473,43 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
   ab.win_div = sums->win_div;
   ab.win_signals = W;
   ab.nwin = nwin;
-  if (p->k1) {
+  // K5's fused ABFT where its registers hold the two window accumulators
+  // without spilling (ptxas -v: FP32 2^5..2^12, FP64 2^5..2^11); K1 otherwise
+  const bool k5abft = p->k5 && p->logn >= 5 && p->logn <= (p->prec == 0 ? 12 : 11) &&
+                      std::getenv("TFFT_NO_K5_ABFT") == nullptr;
+  if (k5abft) {
+    int spt = 1, per_sm = 1;
+    k5_shape(p->prec, p->logn, 1, &spt, &per_sm);
+    const int64_t grid = (int64_t)p->num_sms * per_sm;
+    // pieces of >= SPT signals, ~8 per CTA over the batch
+    int64_t pl = (batch + 8 * grid - 1) / (8 * grid);
+    pl = std::max<int64_t>(spt, (pl + spt - 1) / spt * spt);
+    ab.mode = 1;
+    ab.pieces = std::max<int64_t>(1, (W + pl - 1) / pl);
+    if (ab.pieces > 1) {
+      int e = p->ws.ensure((size_t)nwin * ab.pieces * 2 * p->n * cbytes(p->prec));
+      if (e) return cuda_fail(e, "abft workspace");
+      const size_t cnt_bytes = (size_t)nwin * sizeof(unsigned);
+      if (p->win_count.cap < cnt_bytes) {
+        e = p->win_count.ensure(cnt_bytes);
+        if (e) return cuda_fail(e, "window counters");
+        TFFT_TRY((int)cudaMemsetAsync(p->win_count.p, 0, p->win_count.cap, st), "window counter memset");
+      }
+      ab.ws = p->ws.p;
+      ab.win_count = (unsigned*)p->win_count.p;
+    }
+    K1Args a{};
+    a.x = x;
+    a.y = y;
+    a.batch = batch;
+    a.weight0 = signal_offset;
+    a.tw = p->tw_fwd.p;
+    a.faults = (const DevFault*)p->faults.p;
+    a.nfaults = (int)dev.size();
+    a.counters = (Counters*)counters;
+    a.abft = ab;
+    TFFT_TRY(launch_k5_abft(p->prec, p->logn, a, p->num_sms, st), "k5 abft launch");
+  } else if (p->k1) {
     const int spt = k1_slots(p->prec, p->logn);
     if (W <= 4) {
       ab.mode = 0;

@@ -62,6 +62,10 @@ int launch_k1(int prec, int logn, bool inverse, bool abft, const K1Args& a, int 
 int k1_supported(int prec, int logn);
 // K5: warp-specialised single-pass kernel (same sizes and results as K1's plain path)
 int launch_k5(int prec, int logn, bool inverse, const K1Args& a, int num_sms, cudaStream_t st);
+// K5 with the fused two-sided ABFT (forward only); a.abft.pieces = pieces per window
+int launch_k5_abft(int prec, int logn, const K1Args& a, int num_sms, cudaStream_t st);
+// signals per tile and CTAs per SM of a K5 instantiation (host-side work split)
+void k5_shape(int prec, int logn, int abft, int* spt, int* ctas_per_sm);
 
 }  // namespace tfft
 

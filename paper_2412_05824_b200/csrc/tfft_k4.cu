@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
 #pragma unroll 1
     for (int it = 0;; ++it) {
       const int i = it % K::RR;
-      mbar_wait(&done[i], (it / K::RR) & 1);
+      mbar_wait_sleep(&done[i], (it / K::RR) & 1);
       const long long t = rtk[i];
       if (t < 0) return;
       const K4Item c = k4_decode(a, t);
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
         // by the async proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
-      if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+      if (it >= S) mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
       if (item.phase < 0) {
         tk[s] = -1;
         mbar_arrive(&full[s]);

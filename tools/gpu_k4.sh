@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --timeout 600 > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/tests.log
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/tests.log
 tail -3 $OUT/tests.log
 timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > $OUT/bench.json 2> $OUT/bench.err
 tail -c 2500 $OUT/bench.json
