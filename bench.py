@@ -230,7 +230,8 @@ def run_ours(args, dist):
         gbs = 2 * n * b * 16 / t / 1e9
         sweep.append({"n": n, "batch": b, "ms": round(t * 1e3, 4), "gflops": round(FLOP(n) * b / t / 1e9, 1),
                       "gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
-                      "kernel": "k1_single_pass" if n <= 4096 else "k3_two_pass"})
+                      "kernel": "k1_single_pass" if n <= 256 else ("k5_single_pass" if n <= 4096 else
+                                                                                   "k4_fused_two_pass")})
     dom = max(range(len(sizes)), key=lambda i: statistics.mean(per_n[i]))
     dn = sweep[dom]
     roofline = {"bound": "hbm", "achieved": dn["gbs"], "peak": peak, "unit": "GB/s",
@@ -242,7 +243,8 @@ def run_ours(args, dist):
     if prof.exists():
         tr = json.loads(prof.read_text()).get(str(dn["n"]))
         if tr:
-            roofline["traffic"] = tr
+            roofline["traffic"] = tr["bytes"] if isinstance(tr, dict) else tr
+            roofline["traffic_unit"] = "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
 
     out = {
         "metric": "FFT GFLOP/s (5 N log2 N per transform), C2 FP64 sweep N=2^8..2^20",
@@ -321,7 +323,10 @@ def abft_overheads(args, dist):
         gbs = 2 * n * b * (8 if prec == "single" else 16) / tp / 1e9
         res[name] = {"n": n, "batch_per_gpu": b, "T": T, "bs": plan.bs, "plain_ms": round(tp * 1e3, 4),
                      "fused_ms": round(tfz * 1e3, 4), "overhead_pct": round(100 * (tfz / tp - 1), 2),
-                     "plain_gbs": round(gbs, 1), "path": "fused K1+ABFT" if n <= 4096 else "K3 + device checksum sweeps"}
+                     "plain_gbs": round(gbs, 1),
+                     "path": ("fused K5 (two-sided ABFT in-kernel)" if (prec == "single" or n <= 2048) else
+                              "fused K1 (two-sided ABFT in-kernel)") if n <= 4096 else
+                             "K4 transform + device checksum sweeps"}
         del x, y, sums
         torch.cuda.empty_cache()
     return res

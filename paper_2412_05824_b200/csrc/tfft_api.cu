@@ -125,6 +125,7 @@ struct tfft_plan {
   DevBuf tw_fwd, tw_inv;     // omega_N^k, conj (K1 and ABFT encodings)
   DevBuf enc_tab[2];         // omega_N^k / conj for K3/multipass Jou encoding (lazy)
   DevBuf wsum;               // unfused window sums (s_in, s_out, FFT(s_in))
+  DevBuf part;               // per-(signal, chunk) ABFT partials of the one-sweep path
   DevBuf rows[3];            // left checksum rows per encoding kind
   bool row_ready[3] = {false, false, false};
   DevBuf counters;           // default counters
@@ -415,7 +416,7 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
 
 int tfft_plan_destroy(tfft_plan* p) {
   if (!p) return TFFT_OK;
-  DevBuf* all[] = {&p->tw_fwd, &p->tw_inv, &p->enc_tab[0], &p->enc_tab[1], &p->wsum, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
+  DevBuf* all[] = {&p->part, &p->tw_fwd, &p->tw_inv, &p->enc_tab[0], &p->enc_tab[1], &p->wsum, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
                    &p->ws, &p->win_count, &p->scratch_a, &p->scratch_b, &p->base, &p->col_a, &p->col_b, &p->col64};
   for (DevBuf* b : all) b->release();
   if (p->k3) k3_destroy(p->k3);
@@ -551,23 +552,24 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
       rc = strike_path(p, x, y, batch, 0, signal_offset, slow, st, nullptr);
       if (rc) return rc;
     }
-    TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, 0, batch, p->rows[enc].p, enc_table(p, false), enc, delta, ab,
-                                  (Counters*)counters, 1, st),
-             "row checksums");
     const size_t cb = cbytes(p->prec);
     int e = p->wsum.ensure((size_t)3 * nwin * p->n * cb);
+    if (!e) e = p->part.ensure((size_t)batch * window_sweep_chunks(p->n) * 8 * 5 * sizeof(double));
     if (e) return cuda_fail(e, "window sums");
     char* s_in = (char*)p->wsum.p;
     char* s_out = s_in + (size_t)nwin * p->n * cb;
     char* ref = s_out + (size_t)nwin * p->n * cb;
-    TFFT_TRY(launch_weighted_cols(p->prec, x, p->n, 0, batch, W, signal_offset, s_in, st), "window s_in");
-    TFFT_TRY(launch_weighted_cols(p->prec, y, p->n, 0, batch, W, signal_offset, s_out, st), "window s_out");
+    TFFT_TRY(launch_window_sweep(p->prec, x, y, p->n, batch, W, signal_offset, p->rows[enc].p, enc_table(p, false),
+                                 enc, s_in, s_out, (double*)p->part.p, ab, delta, (Counters*)counters, st),
+             "abft sweep");
     std::vector<DevFault> none;
     int e2 = p->counters.ensure(8 * sizeof(uint64_t));
     if (e2) return cuda_fail(e2, "counters");
     rc = run_plain(p, s_in, ref, nwin, 0, 0, none, (uint64_t*)p->counters.p + 4, st);
     if (rc) return rc;
-    TFFT_TRY(launch_group_div_batched(p->prec, ref, s_out, p->n, nwin, sums->win_div, st), "window group div");
+    // the per-signal partials are consumed (epilogue ran): reuse them for the window partials
+    TFFT_TRY(launch_group_div_chunked(p->prec, ref, s_out, p->n, nwin, sums->win_div, (double*)p->part.p, st),
+             "window group div");
     return TFFT_OK;
   }
   if (slow.empty()) return TFFT_OK;

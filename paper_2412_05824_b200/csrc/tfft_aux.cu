@@ -266,6 +266,132 @@ int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int
 }
 
 // ---------------------------------------------------------------------------
+// one-sweep ABFT sums for the two-pass sizes: a CTA owns (window w, chunk of
+// CH = 256 * V = 1024 elements) and walks the window's signals once, reading x and y
+// exactly once per element. It accumulates the window sums s_in / s_out for
+// its chunk (FP64 FMAs, as weighted_cols) and, per signal, the chunk's
+// partial c_in = row . x, ||x||^2 and c_out = e . y (working precision per
+// thread, FP64 xor tree per warp), written to part[signal][chunk][warp][5]
+// with no barrier in the signal loop; sweep_epilogue adds the partials in
+// (chunk, warp) order per signal.
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 2) window_sweep_kernel(const C<T>* __restrict__ x, const C<T>* __restrict__ y,
+                                                           int64_t n, int64_t batch, int64_t W, int64_t weight0,
+                                                           const C<T>* __restrict__ row, const C<T>* __restrict__ tw,
+                                                           int enc, C<T>* __restrict__ s_in, C<T>* __restrict__ s_out,
+                                                           double* __restrict__ part) {
+  constexpr int CH = 256 * V;
+  const int64_t nchunk = (n + CH - 1) / CH;
+  const int64_t w = blockIdx.x / nchunk, c = blockIdx.x % nchunk;
+  const int64_t j0 = w * W, j1 = min(j0 + W, batch);
+  double ar[V], ai[V], br[V], bi[V];
+  C<T> rw[V], ev[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    ar[i] = ai[i] = br[i] = bi[i] = 0;
+    const int64_t k = c * CH + threadIdx.x + 256 * i;
+    rw[i] = k < n ? row[k] : mk<T>(0, 0);
+    ev[i] = k < n ? enc_value<T>(enc, k, n, tw) : mk<T>(0, 0);
+  }
+#pragma unroll 1
+  for (int64_t j = j0; j < j1; ++j) {
+    const double wj = (double)(weight0 + j + 1);
+    C<T> ci = mk<T>(0, 0), co = mk<T>(0, 0);
+    T fl = 0;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int64_t k = c * CH + threadIdx.x + 256 * i;
+      if (k < n) {
+        const C<T> xv = __ldcs(x + j * n + k), yv = __ldcs(y + j * n + k);
+        ci = cadd<T>(ci, cmul<T>(rw[i], xv));
+        fl = rfma(xv.x, xv.x, rfma(xv.y, xv.y, fl));
+        co = cadd<T>(co, cmul<T>(ev[i], yv));
+        ar[i] = fma(wj, (double)xv.x, ar[i]);
+        ai[i] = fma(wj, (double)xv.y, ai[i]);
+        br[i] = fma(wj, (double)yv.x, br[i]);
+        bi[i] = fma(wj, (double)yv.y, bi[i]);
+      }
+    }
+    // warp partials (fixed xor tree), no CTA barrier inside the signal loop
+    double acc[5] = {(double)ci.x, (double)ci.y, (double)fl, (double)co.x, (double)co.y};
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) part[((j * nchunk + c) * 8 + (threadIdx.x >> 5)) * 5 + q] = acc[q];
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t k = c * CH + threadIdx.x + 256 * i;
+    if (k < n) {
+      s_in[w * n + k] = mk<T>((T)ar[i], (T)ai[i]);
+      s_out[w * n + k] = mk<T>((T)br[i], (T)bi[i]);
+    }
+  }
+}
+
+// one warp per signal: lanes take (chunk, warp) partials i = lane, lane + 32,
+// ... in order, then a fixed xor tree
+__global__ void sweep_epilogue_kernel(const double* __restrict__ part, int64_t nparts, int64_t n, int64_t batch,
+                                      double delta, double* c_in, double* c_out, double* floors, double* div,
+                                      Counters* counters) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < batch; r += nwarps) {
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (int64_t i = lane; i < nparts; i += 32)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc[q] += part[(r * nparts + i) * 5 + q];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+    if (lane != 0) continue;
+    const double floor_v = sqrt(acc[2]) / sqrt((double)n);
+    double dv;
+    if (!isfinite(acc[3]) || !isfinite(acc[4])) dv = __longlong_as_double(0x7ff0000000000000ll);
+    else dv = hypot(acc[0] - acc[3], acc[1] - acc[4]) / fmax(fmax(hypot(acc[0], acc[1]), floor_v), 1e-30);
+    c_in[2 * r] = acc[0];
+    c_in[2 * r + 1] = acc[1];
+    c_out[2 * r] = acc[3];
+    c_out[2 * r + 1] = acc[4];
+    floors[r] = floor_v;
+    div[r] = dv;
+    if (dv > delta) atomicAdd(&counters->triggered, 1ull);
+    atomicMax(&counters->max_div_bits, (unsigned long long)__double_as_longlong(dv));
+  }
+}
+
+int64_t window_sweep_chunks(int64_t n) { return (n + 1023) / 1024; }  // upper bound (FP64 V = 4 -> 1024 per chunk)
+
+int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64_t batch, int64_t W, int64_t weight0,
+                        const void* row, const void* tw, int enc, void* s_in, void* s_out, double* part,
+                        const AbftArgs& ab, double delta, Counters* counters, cudaStream_t st) {
+  const int64_t nwin = (batch + W - 1) / W;
+  const int64_t nchunk = prec == 0 ? (n + 2047) / 2048 : (n + 1023) / 1024;
+  const int64_t blocks = nwin * nchunk;
+  if (blocks <= 0) return 0;
+  if (prec == 0)
+    window_sweep_kernel<float, 8><<<(unsigned)blocks, 256, 0, st>>>(
+        (const float2*)x, (const float2*)y, n, batch, W, weight0, (const float2*)row, (const float2*)tw, enc,
+        (float2*)s_in, (float2*)s_out, part);
+  else
+    window_sweep_kernel<double, 4><<<(unsigned)blocks, 256, 0, st>>>(
+        (const double2*)x, (const double2*)y, n, batch, W, weight0, (const double2*)row, (const double2*)tw, enc,
+        (double2*)s_in, (double2*)s_out, part);
+  int e = (int)cudaGetLastError();
+  if (e) return e;
+  int64_t eb = (batch + 7) / 8;
+  if (eb > 148 * 16) eb = 148 * 16;
+  sweep_epilogue_kernel<<<(unsigned)eb, 256, 0, st>>>(part, nchunk * 8, n, batch, delta, ab.c_in, ab.c_out,
+                                                      ab.floors, ab.div, counters);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // z = a*x + b*y (complex scalars a, b given in FP64; x or y may be null)
 
 template <typename T>
@@ -331,6 +457,56 @@ __global__ void __launch_bounds__(256) group_div_kernel(const C<T>* ref, const C
 
 int launch_group_div(int prec, const void* ref, const void* s_out, int64_t n, double* out, cudaStream_t st) {
   return launch_group_div_batched(prec, ref, s_out, n, 1, out, st);
+}
+
+// chunked group divergence for long rows: partials per (window, 8192-element
+// chunk), then one warp per window adds them in chunk order
+template <typename T>
+__global__ void __launch_bounds__(256) group_div_part_kernel(const C<T>* __restrict__ ref, const C<T>* __restrict__ s_out,
+                                                             int64_t n, int64_t nchunk, double* part) {
+  __shared__ double sh[8 * 2];
+  const int64_t w = blockIdx.x / nchunk, c = blockIdx.x % nchunk;
+  const int64_t k0 = c * 8192, k1 = min(k0 + 8192, n);
+  double acc[2] = {0, 0};
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += 256) {
+    const C<T> r = __ldcs(ref + w * n + k), so = __ldcs(s_out + w * n + k);
+    const double dr = (double)r.x - (double)so.x, di = (double)r.y - (double)so.y;
+    acc[0] += dr * dr + di * di;
+    acc[1] += (double)r.x * (double)r.x + (double)r.y * (double)r.y;
+  }
+  block_sum256<2>(acc, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 2] = acc[0];
+    part[blockIdx.x * 2 + 1] = acc[1];
+  }
+}
+
+__global__ void group_div_fin_kernel(const double* part, int64_t nchunk, int64_t count, double* out) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= count) return;
+  double a = 0, b = 0;
+  for (int64_t c = 0; c < nchunk; ++c) {
+    a += part[(w * nchunk + c) * 2];
+    b += part[(w * nchunk + c) * 2 + 1];
+  }
+  out[w] = sqrt(a) / fmax(sqrt(b), 1e-30);
+}
+
+int launch_group_div_chunked(int prec, const void* ref, const void* s_out, int64_t n, int64_t count, double* out,
+                             double* part, cudaStream_t st) {
+  if (count < 1) return 0;
+  const int64_t nchunk = (n + 8191) / 8192;
+  const int64_t blocks = count * nchunk;
+  if (prec == 0)
+    group_div_part_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float2*)ref, (const float2*)s_out, n, nchunk,
+                                                                   part);
+  else
+    group_div_part_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double2*)ref, (const double2*)s_out, n,
+                                                                    nchunk, part);
+  int e = (int)cudaGetLastError();
+  if (e) return e;
+  group_div_fin_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(part, nchunk, count, out);
+  return (int)cudaGetLastError();
 }
 
 // one CTA per window: row w of ref / s_out -> out[w]

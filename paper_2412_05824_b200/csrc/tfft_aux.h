@@ -17,6 +17,14 @@ int launch_row_checksums(int prec, const void* x, const void* y, int64_t n, int6
                          int count, cudaStream_t st);
 int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int64_t row1, int64_t gsize,
                          int64_t weight0, void* out, cudaStream_t st);
+// one read of x and y: per-signal ABFT sums (via chunk partials + epilogue) and the window sums
+int64_t window_sweep_chunks(int64_t n);
+int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64_t batch, int64_t W, int64_t weight0,
+                        const void* row, const void* tw, int enc, void* s_in, void* s_out, double* part,
+                        const AbftArgs& ab, double delta, Counters* counters, cudaStream_t st);
+// group divergence of `count` long rows through chunk partials (part: count * ceil(n / 8192) * 2 doubles)
+int launch_group_div_chunked(int prec, const void* ref, const void* s_out, int64_t n, int64_t count, double* out,
+                             double* part, cudaStream_t st);
 int launch_axpby(int prec, void* z, int64_t n, double ar, double ai, const void* x, double br, double bi,
                  const void* y, cudaStream_t st);
 int launch_vadd(int prec, void* a, const void* b, int64_t n, cudaStream_t st);

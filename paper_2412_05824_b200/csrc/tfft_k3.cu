@@ -385,8 +385,9 @@ static int k4_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inve
   cudaError_t e = cudaMemsetAsync(p->sync, 0, sync, st);
   if (e != cudaSuccess) return (int)e;
   const int64_t N1 = int64_t(1) << p->l1, N2 = int64_t(1) << p->l2;
-  const int64_t tpa = N2 / k4_columns_per_tile(p->prec, p->l1);  // pass-A tiles per signal
-  const int64_t tpb = N1 / k4_columns_per_tile(p->prec, p->l2);
+  const int lmax = p->l1 > p->l2 ? p->l1 : p->l2;
+  const int64_t tpa = N2 / k4_columns_per_tile(p->prec, p->l1, lmax);  // pass-A tiles per signal
+  const int64_t tpb = N1 / k4_columns_per_tile(p->prec, p->l2, lmax);
   const int64_t glast = batch - (ng - 1) * G;
   const int c = inverse ? 1 : 0;
   K4Args a{};

@@ -440,22 +440,30 @@ static int launch_k4_t(const K4Args& a, int num_sms, cudaStream_t st) {
 // production tile shapes: 16 elements x 128 consumer threads (2048-element
 // tiles) and two CTAs per SM, so one CTA's exchange barriers overlap the
 // other's radix arithmetic
-template <typename T> struct K4Shape;
-template <> struct K4Shape<double> { static constexpr int E = 16, NT = 128, S = 1, MINB = 2; };
-template <> struct K4Shape<float> { static constexpr int E = 16, NT = 256, S = 2, MINB = 1; };
+// (FP32: 128-consumer CTAs measured faster up to 256-point columns, 256 beyond)
+template <typename T, int LMAX> struct K4Shape;
+template <int LMAX> struct K4Shape<double, LMAX> { static constexpr int E = 16, NT = 128, S = 1, MINB = 2; };
+template <int LMAX> struct K4Shape<float, LMAX> {
+  static constexpr int E = 16, NT = LMAX <= 8 ? 128 : 256, S = LMAX <= 8 ? 3 : 2, MINB = 2;
+};
 
 template <typename T>
-int k4_tile_cols(int logl) {
-  return K4Shape<T>::NT / ((1 << logl) / K4Shape<T>::E);
+int k4_tile_cols(int logl, int lmax) {
+  const int nt = lmax <= 8 ? K4Shape<T, 8>::NT : K4Shape<T, 11>::NT;
+  return nt / ((1 << logl) / K4Shape<T, 8>::E);
 }
 
-int k4_columns_per_tile(int prec, int logl) { return prec == 0 ? k4_tile_cols<float>(logl) : k4_tile_cols<double>(logl); }
+int k4_columns_per_tile(int prec, int logl, int lmax) {
+  return prec == 0 ? k4_tile_cols<float>(logl, lmax) : k4_tile_cols<double>(logl, lmax);
+}
 
 template <typename T, bool INV>
 static int dispatch_k4(int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
-  constexpr int E = K4Shape<T>::E, NT = K4Shape<T>::NT, S = K4Shape<T>::S, MINB = K4Shape<T>::MINB;
-#define TFFT_K4(A, B) \
-  if (l1 == A && l2 == B) return launch_k4_t<T, A, B, INV, E, NT, S, MINB>(a, num_sms, st);
+#define TFFT_K4(A, B)                                                                                   \
+  if (l1 == A && l2 == B) {                                                                             \
+    using SH = K4Shape<T, (A > B ? A : B)>;                                                             \
+    return launch_k4_t<T, A, B, INV, SH::E, SH::NT, SH::S, SH::MINB>(a, num_sms, st);                   \
+  }
   TFFT_K4_PAIRS
 #undef TFFT_K4
   return (int)cudaErrorInvalidValue;
@@ -465,7 +473,8 @@ static int dispatch_k4(int l1, int l2, const K4Args& a, int num_sms, cudaStream_
 // least 16 bytes (CB columns of complex values)
 template <typename T>
 static bool k4_shape_ok(int l1, int l2) {
-  return 2 * k4_tile_cols<T>(l1) * (int)sizeof(T) >= 16 && 2 * k4_tile_cols<T>(l2) * (int)sizeof(T) >= 16;
+  const int lmax = l1 > l2 ? l1 : l2;
+  return 2 * k4_tile_cols<T>(l1, lmax) * (int)sizeof(T) >= 16 && 2 * k4_tile_cols<T>(l2, lmax) * (int)sizeof(T) >= 16;
 }
 
 bool k4_supported(int prec, int l1, int l2) {

@@ -40,7 +40,7 @@ struct K4Args {
 };
 
 bool k4_supported(int prec, int l1, int l2);
-int k4_columns_per_tile(int prec, int logl);
+int k4_columns_per_tile(int prec, int logl, int lmax);
 int launch_k4(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
 
 }  // namespace tfft
