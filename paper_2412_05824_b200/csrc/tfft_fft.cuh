@@ -25,6 +25,18 @@ __device__ __forceinline__ void fft_sync() {
   else asm volatile("bar.sync 1, %0;" ::"n"(BAR_THREADS) : "memory");
 }
 
+// Exchange synchronisation of one signal's TPS threads. BAR_THREADS >= 0: as
+// fft_sync. BAR_THREADS == -1 ("group" mode, tau-fastest thread maps): a
+// signal whose threads fit in one warp syncs with __syncwarp; a wider one
+// uses named barrier `bar_id` over its own TPS threads only, so signals (and
+// warps) of one CTA never wait for each other.
+template <int BAR_THREADS, int TPS>
+__device__ __forceinline__ void fft_sync_grp(int bar_id) {
+  if constexpr (BAR_THREADS >= 0) fft_sync<BAR_THREADS>();
+  else if constexpr (TPS <= 32) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(TPS) : "memory");
+}
+
 // PF: issue the next pass's twiddle loads before the exchange barriers so their
 // L1/L2 latency hides behind the shared-memory round trip (costs E registers).
 // TWS: where the twiddles come from.
@@ -155,17 +167,17 @@ struct Fft {
   }
 
   template <int P>
-  static __device__ __forceinline__ void rest(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw) {
+  static __device__ __forceinline__ void rest(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw, int bar_id) {
     if constexpr (P < NPASS) {
       C<T> w[E];
       if constexpr (PF) load_tw<P>(w, tau, tw);
-      fft_sync<BAR_THREADS>();
+      fft_sync_grp<BAR_THREADS, TPS>(bar_id);
       write<P - 1>(buf, v, tau);
-      fft_sync<BAR_THREADS>();
+      fft_sync_grp<BAR_THREADS, TPS>(bar_id);
       read<P>(buf, v, tau);
       if constexpr (!PF) load_tw<P>(w, tau, tw);
       apply<P>(v, w);
-      rest<P + 1>(buf, v, tau, tw);
+      rest<P + 1>(buf, v, tau, tw, bar_id);
     }
   }
 
@@ -174,9 +186,10 @@ struct Fft {
   // smem read is complete for this thread but the caller must barrier before
   // overwriting buf. Contains NPASS-1 pairs of CTA-wide barriers: every thread
   // must call it. buf spans NPAD elements (padded layout).
-  static __device__ __forceinline__ void run(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw) {
+  // bar_id: the named barrier of this signal's thread group in group mode
+  static __device__ __forceinline__ void run(C<T>* buf, C<T> (&v)[E], int tau, const C<T>* tw, int bar_id = 1) {
     compute<0>(v, tau, tw);
-    rest<1>(buf, v, tau, tw);
+    rest<1>(buf, v, tau, tw, bar_id);
   }
 };
 

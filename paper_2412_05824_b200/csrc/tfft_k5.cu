@@ -38,7 +38,8 @@ struct K5 {
   static constexpr int S0 = 100 * 1024 / TILE_BYTES0;
   static constexpr int S = S0 < 2 ? 2 : (S0 > 4 ? 4 : S0);
   static constexpr bool TWS = N * BPC <= 65536 && (S + (ABFT ? 1 : 0)) * TILE_BYTES0 + N * BPC <= 210 * 1024;
-  using F = Fft<T, N, EMAX, INV, false, NT, TWS>;
+  // group-mode exchanges: a signal's TPS threads sync among themselves only
+  using F = Fft<T, N, EMAX, INV, false, -1, TWS>;
   static constexpr int E = F::E;
   static constexpr int TPS = F::TPS;
   static constexpr int SPT = NT / TPS;  // signals per tile
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NT + 32, K5<T, LOGN, I
             }
         }
       }
-      F::run(buf, v, tau, tw);
+      F::run(buf, v, tau, tw, 2 + g);
       // this warp's reads of the slot are complete: hand it back to the
       // producer (generic-proxy writes ordered before the next bulk copy)
       fence_proxy_async();
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NT + 32, K5<T, LOGN, I
 #pragma unroll
         for (int k = 0; k < E; ++k) vv[k] = have ? s_in[k] : mk<T>(0, 0);
         CT* wb = wbuf + g * K::SLOT;
-        F::run(wb, vv, tau, tw);
+        F::run(wb, vv, tau, tw, 2 + g);
         // s_out of slot 0 is at natural positions: fetch the ones matching the
         // output positions through the (now free) window buffer
         fft_sync<NT>();
