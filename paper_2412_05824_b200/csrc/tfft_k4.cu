@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
     for (int it = 0;; ++it) {
       const int s = it % S;
       if (item.phase >= 0) {
-        while (!k4_ready(a, item)) __nanosleep(32);
+        while (!k4_ready(a, item)) __nanosleep(256);
         // the tile (pass B: written by other CTAs' generic stores) is read
         // by the async proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");
