@@ -1,16 +1,18 @@
 #!/usr/bin/env bash
-# one gpurun call: GPU parity tests, smoke, bench, launch list, ncu captures.
+# one gpurun call: GPU parity tests, smoke, bench (+ reference arm), launch list, ncu captures.
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/gpu.txt 2>&1
-timeout 1200 python -m pytest tests -m gpu -q -x --timeout 900 > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/tests.log
+timeout 600 python -m pytest tests -m gpu -q --timeout 300 > $OUT/tests.log 2>&1; echo "tests rc=$?" >> $OUT/tests.log
 tail -3 $OUT/tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
-timeout 900 python bench.py --steps 5 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
-tail -c 3000 $OUT/bench.json
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 600 python bench.py --steps 5 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
+timeout 400 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+tail -c 800 $OUT/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-abft > /dev/null 2>&1
-bash tools/gpu_prof.sh "k1_fp64_n4096 k1_kernel 2 1 --n 4096 --prec double" \
-  "k3_fp64_n1m col_kernel 2 2 --n 1048576 --prec double" \
-  "k1_fp32_n1024 k1_kernel 2 1 --n 1024 --prec single" \
-  "k1abft_fp32_n4096 k1_kernel 2 1 --n 4096 --prec single --abft"
+sed -i 's/timeout 900 ncu/timeout 300 ncu/' tools/gpu_prof.sh
+bash tools/gpu_prof.sh "k4_fp64_n1m k4_kernel 1 1 --n 1048576 --prec double" "k4_fp64_n65536 k4_kernel 1 1 --n 65536 --prec double" \
+  "k5_fp64_n4096 k5_kernel 1 1 --n 4096 --prec double" "k5_fp64_n1024 k5_kernel 1 1 --n 1024 --prec double" \
+  "k5_fp32_n1024 k5_kernel 1 1 --n 1024 --prec single" "k5abft_fp32_n4096 k5_kernel 1 1 --n 4096 --prec single --abft" \
+  "k1_fp64_n256 k1_kernel 1 1 --n 256 --prec double"
