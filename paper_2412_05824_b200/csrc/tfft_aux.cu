@@ -269,7 +269,7 @@ int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int
 // one-sweep ABFT sums for the two-pass sizes: a CTA owns (window w, chunk of
 // CH = 256 * V = 1024 elements) and walks the window's signals once, reading x and y
 // exactly once per element. It accumulates the window sums s_in / s_out for
-// its chunk (FP64 FMAs, as weighted_cols) and, per signal, the chunk's
+// its chunk (working precision, as the reference's GEMV) and, per signal, the chunk's
 // partial c_in = row . x, ||x||^2 and c_out = e . y (working precision per
 // thread, FP64 xor tree per warp), written to part[signal][chunk][warp][5]
 // with no barrier in the signal loop; sweep_epilogue adds the partials in
@@ -277,41 +277,49 @@ int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int
 
 template <typename T, int V>
 __global__ void __launch_bounds__(256, 2) window_sweep_kernel(const C<T>* __restrict__ x, const C<T>* __restrict__ y,
-                                                           int64_t n, int64_t batch, int64_t W, int64_t weight0,
-                                                           const C<T>* __restrict__ row, const C<T>* __restrict__ tw,
-                                                           int enc, C<T>* __restrict__ s_in, C<T>* __restrict__ s_out,
-                                                           double* __restrict__ part) {
+                                                        int64_t n, int64_t batch, int64_t W, int64_t weight0,
+                                                        const C<T>* __restrict__ row, const C<T>* __restrict__ tw,
+                                                        int enc, C<T>* __restrict__ s_in, C<T>* __restrict__ s_out,
+                                                        double* __restrict__ part) {
   constexpr int CH = 256 * V;
   const int64_t nchunk = (n + CH - 1) / CH;
   const int64_t w = blockIdx.x / nchunk, c = blockIdx.x % nchunk;
   const int64_t j0 = w * W, j1 = min(j0 + W, batch);
-  double ar[V], ai[V], br[V], bi[V];
-  C<T> rw[V], ev[V];
+  const int64_t kb = c * CH + threadIdx.x;
+  // window sums in working precision, as the reference's GEMV (abft.py:605-606)
+  C<T> a_in[V], a_out[V], rw[V], ev[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    ar[i] = ai[i] = br[i] = bi[i] = 0;
-    const int64_t k = c * CH + threadIdx.x + 256 * i;
+    a_in[i] = a_out[i] = mk<T>(0, 0);
+    const int64_t k = kb + 256 * i;
     rw[i] = k < n ? row[k] : mk<T>(0, 0);
     ev[i] = k < n ? enc_value<T>(enc, k, n, tw) : mk<T>(0, 0);
   }
+  // loads of the next signal are issued before the current one is reduced
+  C<T> xv[V], yv[V];
+  auto load = [&](int64_t j, C<T>(&xa)[V], C<T>(&ya)[V]) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int64_t k = kb + 256 * i;
+      xa[i] = (j < j1 && k < n) ? __ldcs(x + j * n + k) : mk<T>(0, 0);
+      ya[i] = (j < j1 && k < n) ? __ldcs(y + j * n + k) : mk<T>(0, 0);
+    }
+  };
+  load(j0, xv, yv);
 #pragma unroll 1
   for (int64_t j = j0; j < j1; ++j) {
-    const double wj = (double)(weight0 + j + 1);
+    C<T> xn[V], yn[V];
+    load(j + 1, xn, yn);
+    const T wj = (T)(weight0 + j + 1);
     C<T> ci = mk<T>(0, 0), co = mk<T>(0, 0);
     T fl = 0;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const int64_t k = c * CH + threadIdx.x + 256 * i;
-      if (k < n) {
-        const C<T> xv = __ldcs(x + j * n + k), yv = __ldcs(y + j * n + k);
-        ci = cadd<T>(ci, cmul<T>(rw[i], xv));
-        fl = rfma(xv.x, xv.x, rfma(xv.y, xv.y, fl));
-        co = cadd<T>(co, cmul<T>(ev[i], yv));
-        ar[i] = fma(wj, (double)xv.x, ar[i]);
-        ai[i] = fma(wj, (double)xv.y, ai[i]);
-        br[i] = fma(wj, (double)yv.x, br[i]);
-        bi[i] = fma(wj, (double)yv.y, bi[i]);
-      }
+      ci = cadd<T>(ci, cmul<T>(rw[i], xv[i]));
+      fl = rfma(xv[i].x, xv[i].x, rfma(xv[i].y, xv[i].y, fl));
+      co = cadd<T>(co, cmul<T>(ev[i], yv[i]));
+      a_in[i] = mk<T>(rfma(wj, xv[i].x, a_in[i].x), rfma(wj, xv[i].y, a_in[i].y));
+      a_out[i] = mk<T>(rfma(wj, yv[i].x, a_out[i].x), rfma(wj, yv[i].y, a_out[i].y));
     }
     // warp partials (fixed xor tree), no CTA barrier inside the signal loop
     double acc[5] = {(double)ci.x, (double)ci.y, (double)fl, (double)co.x, (double)co.y};
@@ -322,13 +330,18 @@ __global__ void __launch_bounds__(256, 2) window_sweep_kernel(const C<T>* __rest
     if ((threadIdx.x & 31) == 0)
 #pragma unroll
       for (int q = 0; q < 5; ++q) part[((j * nchunk + c) * 8 + (threadIdx.x >> 5)) * 5 + q] = acc[q];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      xv[i] = xn[i];
+      yv[i] = yn[i];
+    }
   }
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const int64_t k = c * CH + threadIdx.x + 256 * i;
+    const int64_t k = kb + 256 * i;
     if (k < n) {
-      s_in[w * n + k] = mk<T>((T)ar[i], (T)ai[i]);
-      s_out[w * n + k] = mk<T>((T)br[i], (T)bi[i]);
+      s_in[w * n + k] = a_in[i];
+      s_out[w * n + k] = a_out[i];
     }
   }
 }
@@ -365,21 +378,21 @@ __global__ void sweep_epilogue_kernel(const double* __restrict__ part, int64_t n
   }
 }
 
-int64_t window_sweep_chunks(int64_t n) { return (n + 1023) / 1024; }  // upper bound (FP64 V = 4 -> 1024 per chunk)
+int64_t window_sweep_chunks(int64_t n) { return (n + 511) / 512; }  // upper bound (FP64 V = 2 -> 512 per chunk)
 
 int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64_t batch, int64_t W, int64_t weight0,
                         const void* row, const void* tw, int enc, void* s_in, void* s_out, double* part,
                         const AbftArgs& ab, double delta, Counters* counters, cudaStream_t st) {
   const int64_t nwin = (batch + W - 1) / W;
-  const int64_t nchunk = prec == 0 ? (n + 2047) / 2048 : (n + 1023) / 1024;
+  const int64_t nchunk = prec == 0 ? (n + 1023) / 1024 : (n + 511) / 512;
   const int64_t blocks = nwin * nchunk;
   if (blocks <= 0) return 0;
   if (prec == 0)
-    window_sweep_kernel<float, 8><<<(unsigned)blocks, 256, 0, st>>>(
+    window_sweep_kernel<float, 4><<<(unsigned)blocks, 256, 0, st>>>(
         (const float2*)x, (const float2*)y, n, batch, W, weight0, (const float2*)row, (const float2*)tw, enc,
         (float2*)s_in, (float2*)s_out, part);
   else
-    window_sweep_kernel<double, 4><<<(unsigned)blocks, 256, 0, st>>>(
+    window_sweep_kernel<double, 2><<<(unsigned)blocks, 256, 0, st>>>(
         (const double2*)x, (const double2*)y, n, batch, W, weight0, (const double2*)row, (const double2*)tw, enc,
         (double2*)s_in, (double2*)s_out, part);
   int e = (int)cudaGetLastError();
