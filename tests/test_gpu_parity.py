@@ -243,3 +243,30 @@ def test_fused_two_pass_many_groups(precision, log2n, groups):
         assert np.array_equal(part, y[sel])
     back = tf.execute_plan(plan, tf.SignalBatch(y), "inverse").data
     assert max_rel_error(back, x) <= (1e-5 if precision == "single" else 1e-12)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_batch_pipelined_bitwise(pinned):
+    """Large host batches stream through H2D / transform / D2H in chunks
+    (fft_core._execute_host_pipelined): bitwise equal to the device-resident
+    transform, for pinned and pageable buffers, with a short last chunk."""
+    import torch
+    tf = _tf()
+    from paper_2412_05824_b200 import fft_core
+    n, b = 4096, 2100  # 65.6 MiB FP32 -> two chunks, the second short
+    x = gaussian(n, b, "single", seed=11)
+    if pinned:
+        hx = torch.from_numpy(x).pin_memory()
+        x = hx.numpy()
+        hy = torch.empty_like(hx).pin_memory()
+        out = hy.numpy()
+    else:
+        out = None
+    plan = tf.build_plan(tf.select_params(n, b, "single"), "single")
+    assert x.nbytes >= fft_core._PIPELINE_MIN_BYTES
+    got = tf.execute_plan(plan, tf.SignalBatch(x), out=out).data
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    ref = tf.execute_plan(plan, tf.SignalBatch(xd)).data.cpu().numpy()
+    assert np.array_equal(got, ref)
+    back = tf.execute_plan(plan, tf.SignalBatch(got), "inverse").data
+    assert max_rel_error(back, x) <= 1e-5
