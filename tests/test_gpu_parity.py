@@ -270,3 +270,18 @@ def test_host_batch_pipelined_bitwise(pinned):
     assert np.array_equal(got, ref)
     back = tf.execute_plan(plan, tf.SignalBatch(got), "inverse").data
     assert max_rel_error(back, x) <= 1e-5
+
+
+@pytest.mark.parametrize("precision,n,b", [("double", 1024, 5), ("single", 4096, 3), ("double", 65536, 3),
+                                           ("single", 16384, 40), ("single", 4096, 4200)])
+def test_nonfinite_input_rejected_every_kernel(precision, n, b):
+    """K5, K4 and the chunked host pipeline all raise on a non-finite input
+    (fft_core.py:283-306), plain and protected."""
+    tf = _tf()
+    x = gaussian(n, b, precision, seed=2)
+    x[b - 1, n // 2] = complex(np.nan, 0.0)
+    plan = tf.build_plan(tf.select_params(n, b, precision), precision)
+    with pytest.raises(ValueError):
+        tf.execute_plan(plan, tf.SignalBatch(x))
+    with pytest.raises(ValueError):
+        tf.run_protected(plan, tf.SignalBatch(x), group_size=2)
