@@ -359,8 +359,60 @@ static int64_t k4_group(const K3Plan* p, int64_t batch) {
   return g;
 }
 
+static int k4_execute_chunk(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults,
+                            int nfaults, Counters* counters, cudaStream_t st);
+
+// TMA coordinates are 32-bit: x is addressed as batch * N1 rows (and y as
+// batch * N2 rows), so very large batches run as several launches of at most
+// 2^31 / max(N1, N2) signals each (faults are re-based per chunk)
 static int k4_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults,
                       int nfaults, Counters* counters, cudaStream_t st) {
+  const int64_t rows = int64_t(1) << (p->l1 > p->l2 ? p->l1 : p->l2);
+  int64_t maxb = (int64_t(1) << 31) / rows - 1;
+  if (const char* env = std::getenv("TFFT_K4_MAX_BATCH")) {  // test hook: force the chunked path
+    const long long v = std::atoll(env);
+    if (v > 0 && v < maxb) maxb = v;
+  }
+  if (batch <= maxb) return k4_execute_chunk(p, x, y, batch, inverse, faults, nfaults, counters, st);
+  const size_t cb = p->prec == 0 ? 8 : 16;
+  std::vector<DevFault> host(nfaults);
+  if (nfaults) {
+    cudaError_t e = cudaMemcpy(host.data(), faults, nfaults * sizeof(DevFault), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return (int)e;
+  }
+  DevFault* dfl = nullptr;
+  if (nfaults) {
+    cudaError_t e = cudaMalloc(&dfl, nfaults * sizeof(DevFault));
+    if (e != cudaSuccess) return (int)e;
+  }
+  int rc = 0;
+  for (int64_t b0 = 0; b0 < batch && !rc; b0 += maxb) {
+    const int64_t nb = batch - b0 < maxb ? batch - b0 : maxb;
+    std::vector<DevFault> mine;
+    for (const DevFault& f : host)
+      if (f.signal >= b0 && f.signal < b0 + nb) {
+        DevFault g = f;
+        g.signal -= b0;
+        mine.push_back(g);
+      }
+    if (!mine.empty()) {
+      cudaError_t e = cudaMemcpyAsync(dfl, mine.data(), mine.size() * sizeof(DevFault), cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) {
+        rc = (int)e;
+        break;
+      }
+    }
+    rc = k4_execute_chunk(p, static_cast<const char*>(x) + (size_t)b0 * p->n * cb,
+                          static_cast<char*>(y) + (size_t)b0 * p->n * cb, nb, inverse, mine.empty() ? nullptr : dfl,
+                          (int)mine.size(), counters, st);
+    if (!mine.empty()) cudaStreamSynchronize(st);  // dfl is reused by the next chunk
+  }
+  cudaFree(dfl);
+  return rc;
+}
+
+static int k4_execute_chunk(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults,
+                            int nfaults, Counters* counters, cudaStream_t st) {
   const size_t cb = p->prec == 0 ? 8 : 16;
   const int64_t G = k4_group(p, batch);
   const size_t ring = (size_t)3 * G * p->n * cb;
