@@ -321,15 +321,16 @@ __global__ void __launch_bounds__(256, 2) window_sweep_kernel(const C<T>* __rest
       a_in[i] = mk<T>(rfma(wj, xv[i].x, a_in[i].x), rfma(wj, xv[i].y, a_in[i].y));
       a_out[i] = mk<T>(rfma(wj, yv[i].x, a_out[i].x), rfma(wj, yv[i].y, a_out[i].y));
     }
-    // warp partials (fixed xor tree), no CTA barrier inside the signal loop
-    double acc[5] = {(double)ci.x, (double)ci.y, (double)fl, (double)co.x, (double)co.y};
+    // warp partials: fixed xor tree in working precision (the products are
+    // working precision already), no CTA barrier inside the signal loop
+    T acc[5] = {ci.x, ci.y, fl, co.x, co.y};
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1)
 #pragma unroll
-      for (int q = 0; q < 5; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+      for (int q = 0; q < 5; ++q) acc[q] = radd(acc[q], __shfl_xor_sync(0xffffffffu, acc[q], off));
     if ((threadIdx.x & 31) == 0)
 #pragma unroll
-      for (int q = 0; q < 5; ++q) part[((j * nchunk + c) * 8 + (threadIdx.x >> 5)) * 5 + q] = acc[q];
+      for (int q = 0; q < 5; ++q) part[((j * nchunk + c) * 8 + (threadIdx.x >> 5)) * 5 + q] = (double)acc[q];
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       xv[i] = xn[i];
@@ -384,11 +385,11 @@ int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64
                         const void* row, const void* tw, int enc, void* s_in, void* s_out, double* part,
                         const AbftArgs& ab, double delta, Counters* counters, cudaStream_t st) {
   const int64_t nwin = (batch + W - 1) / W;
-  const int64_t nchunk = prec == 0 ? (n + 1023) / 1024 : (n + 511) / 512;
+  const int64_t nchunk = prec == 0 ? (n + 2047) / 2048 : (n + 511) / 512;
   const int64_t blocks = nwin * nchunk;
   if (blocks <= 0) return 0;
   if (prec == 0)
-    window_sweep_kernel<float, 4><<<(unsigned)blocks, 256, 0, st>>>(
+    window_sweep_kernel<float, 8><<<(unsigned)blocks, 256, 0, st>>>(
         (const float2*)x, (const float2*)y, n, batch, W, weight0, (const float2*)row, (const float2*)tw, enc,
         (float2*)s_in, (float2*)s_out, part);
   else
