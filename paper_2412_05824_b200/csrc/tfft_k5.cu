@@ -315,10 +315,17 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NT + 32, K5<T, LOGN, I
         // warp; for TPS > 32 the slot's warps publish partials and the last one
         // to arrive (shared-memory counter) adds them in warp order
         constexpr int W0 = TPS < 32 ? TPS : 32;
+        {
+          // lane tree in working precision (the partials are working precision
+          // already; halves the shuffles for FP32), then FP64 across warps
+          T r5[5] = {(T)red5[0], (T)red5[1], (T)red5[2], (T)red5[3], (T)red5[4]};
 #pragma unroll
-        for (int off = W0 / 2; off >= 1; off >>= 1)
+          for (int off = W0 / 2; off >= 1; off >>= 1)
 #pragma unroll
-          for (int kk = 0; kk < 5; ++kk) red5[kk] += __shfl_xor_sync(0xffffffffu, red5[kk], off);
+            for (int kk = 0; kk < 5; ++kk) r5[kk] = radd(r5[kk], __shfl_xor_sync(0xffffffffu, r5[kk], off));
+#pragma unroll
+          for (int kk = 0; kk < 5; ++kk) red5[kk] = (double)r5[kk];
+        }
         bool fin = valid && tau == 0;
         if constexpr (TPS > 32) {
           constexpr int NW = TPS / 32;
