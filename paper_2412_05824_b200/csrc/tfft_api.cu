@@ -474,9 +474,9 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
   ab.win_div = sums->win_div;
   ab.win_signals = W;
   ab.nwin = nwin;
-  // K5's fused ABFT where its registers hold the two window accumulators
-  // without spilling (ptxas -v: FP32 2^5..2^12, FP64 2^5..2^11); K1 otherwise
-  const bool k5abft = p->k5 && p->logn >= 5 && p->logn <= (p->prec == 0 ? 12 : 11) &&
+  // K5's fused ABFT (FP64 2^12 runs its inline-producer variant so the
+  // window accumulators fit the register budget); K1 otherwise
+  const bool k5abft = p->k5 && p->logn >= 5 && p->logn <= 12 &&
                       std::getenv("TFFT_NO_K5_ABFT") == nullptr;
   if (k5abft) {
     int spt = 1, per_sm = 1;

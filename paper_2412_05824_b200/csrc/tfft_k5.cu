@@ -52,6 +52,12 @@ struct K5 {
   // ABFT keeps two window accumulators (E complex each) per thread beside the
   // E legs: FP64 needs the whole register file of one CTA per SM for them
   static constexpr int MINB = (ABFT && sizeof(T) == 8) ? 1 : (NT <= 128 ? 2 : 1);
+  // FP64 ABFT with a 256-thread signal: no separate producer warp (thread 0
+  // refills the freed stage after a consumer barrier, as K1 does), so the
+  // eight consumer warps keep the whole 255-register budget for the legs and
+  // the two window accumulators
+  static constexpr bool INL = ABFT && sizeof(T) == 8 && NT >= 256;
+  static constexpr int NTHR = NT + (INL ? 0 : 32);
   static constexpr int NWARP_SLOT = TPS >= 32 ? TPS / 32 : 1;
   // per-signal partials: 2 tile parities x SPT slots x warps x 5 doubles + arrival counters
   static constexpr int RED_BYTES = ABFT ? (2 * SPT * NWARP_SLOT * 5 * 8 + 2 * SPT * 4 + 8) : 0;
@@ -102,7 +108,7 @@ __device__ __forceinline__ void k5_slot_reduce(double (&r)[NV], double* red, int
 // slots are combined in order; a window split into P > 1 pieces is finished
 // by its last-arriving piece, which adds the piece partials in piece order.
 template <typename T, int LOGN, bool INV, bool ABFT>
-__global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NT + 32, K5<T, LOGN, INV, ABFT>::MINB)
+__global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV, ABFT>::MINB)
     k5_kernel(K1Args a) {
   using K = K5<T, LOGN, INV, ABFT>;
   using F = typename K::F;
@@ -145,44 +151,59 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NT + 32, K5<T, LOGN, I
     }
     fence_mbar_init();
   }
-  if constexpr (K::TWS) F::build_pass_tables(tws, static_cast<const CT*>(a.tw), tid, NT + 32);
+  if constexpr (K::TWS) F::build_pass_tables(tws, static_cast<const CT*>(a.tw), tid, K::NTHR);
   if constexpr (K::ROWS) {
     const CT* gr = static_cast<const CT*>(a.abft.row);
-    for (int i = tid; i < N; i += NT + 32) rows[i] = gr[i];
+    for (int i = tid; i < N; i += K::NTHR) rows[i] = gr[i];
   }
   if constexpr (ABFT) {
     int* cnt = reinterpret_cast<int*>(red + 2 * SPT * K::NWARP_SLOT * 5);
-    for (int i = tid; i < 2 * SPT; i += NT + 32) cnt[i] = 0;
+    for (int i = tid; i < 2 * SPT; i += K::NTHR) cnt[i] = 0;
   }
   __syncthreads();
   const CT* tw = K::TWS ? tws : static_cast<const CT*>(a.tw);
 
-  if (tid >= NT) {
-    // ------------------------------------------------------------ producer
-    if (tid != NT) return;
-    int it = 0;
+  // the it-th tile this CTA loads: item cursor (p_item, p_i); lands in stage it % S
+  int64_t p_item = blockIdx.x, p_i = 0;
+  int p_it = 0;
+  auto produce_next = [&]() {  // one thread
 #pragma unroll 1
-    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    while (p_item < nitems) {
       int64_t ps, pe;
-      piece(item, ps, pe);
+      piece(p_item, ps, pe);
       // at least one tile per item: an empty piece (short last window) still
       // has to arrive for its window to be finished
       const int64_t ntl = pe > ps ? (pe - ps + SPT - 1) / SPT : 1;
-#pragma unroll 1
-      for (int64_t i = 0; i < ntl; ++i, ++it) {
-        const int s = it % S;
-        if (it >= S) mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
-        const int64_t s0 = ps + i * SPT;
-        const int nsig = (int)(pe - s0 <= 0 ? 0 : (pe - s0 < SPT ? pe - s0 : SPT));
-        CT* dst = ring + s * K::TILE;
-        if (nsig == 0) {
-          k5_arrive(&full[s]);
-        } else {
-          mbar_expect_tx(&full[s], (uint32_t)(nsig * N * K::BPC));
-          for (int gg = 0; gg < nsig; ++gg)
-            bulk_g2s(dst + gg * K::SLOT, x + (s0 + gg) * N, N * K::BPC, &full[s]);
-        }
+      if (p_i >= ntl) {
+        p_item += gridDim.x;
+        p_i = 0;
+        continue;
       }
+      const int s = p_it % S;
+      const int64_t s0 = ps + p_i * SPT;
+      const int nsig = (int)(pe - s0 <= 0 ? 0 : (pe - s0 < SPT ? pe - s0 : SPT));
+      CT* dst = ring + s * K::TILE;
+      if (nsig == 0) {
+        k5_arrive(&full[s]);
+      } else {
+        mbar_expect_tx(&full[s], (uint32_t)(nsig * N * K::BPC));
+        for (int gg = 0; gg < nsig; ++gg) bulk_g2s(dst + gg * K::SLOT, x + (s0 + gg) * N, N * K::BPC, &full[s]);
+      }
+      ++p_i;
+      ++p_it;
+      return;
+    }
+  };
+  if constexpr (K::INL) {
+    if (tid == 0)
+      for (int i = 0; i < S; ++i) produce_next();
+  } else if (tid >= NT) {
+    // ------------------------------------------------------------ producer
+    if (tid != NT) return;
+#pragma unroll 1
+    while (p_item < nitems) {
+      if (p_it >= S) mbar_wait_sleep(&empty[p_it % S], ((p_it / S) & 1) ^ 1);
+      produce_next();
     }
     return;
   }
@@ -256,8 +277,13 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NT + 32, K5<T, LOGN, I
       // this warp's reads of the slot are complete: hand it back to the
       // producer (generic-proxy writes ordered before the next bulk copy)
       fence_proxy_async();
-      __syncwarp();
-      if ((tid & 31) == 0) k5_arrive(&empty[s]);
+      if constexpr (K::INL) {
+        fft_sync<NT>();  // every consumer is done with stage s: refill it
+        if (tid == 0) produce_next();
+      } else {
+        __syncwarp();
+        if ((tid & 31) == 0) k5_arrive(&empty[s]);
+      }
       if constexpr (INV) {
         const T sc = (T)(1.0 / (double)N);
 #pragma unroll
@@ -481,7 +507,7 @@ static int launch_k5_t(const K1Args& a, int num_sms, cudaStream_t st) {
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT + 32, K::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NTHR, K::SMEM);
     if (e != cudaSuccess) return (int)e;
     if (per_sm < 1) per_sm = 1;
     configured = true;
@@ -490,7 +516,7 @@ static int launch_k5_t(const K1Args& a, int num_sms, cudaStream_t st) {
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > nitems) grid = nitems;
   if (grid < 1) return 0;
-  kern<<<(unsigned)grid, K::NT + 32, K::SMEM, st>>>(a);
+  kern<<<(unsigned)grid, K::NTHR, K::SMEM, st>>>(a);
   return (int)cudaGetLastError();
 }
 
