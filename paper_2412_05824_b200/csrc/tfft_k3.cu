@@ -465,6 +465,8 @@ static int k4_execute_chunk(K3Plan* p, const void* x, void* y, int64_t batch, in
   a.ticket = static_cast<unsigned long long*>(p->sync);
   a.done_a = reinterpret_cast<unsigned*>(static_cast<char*>(p->sync) + 8);
   a.done_b = a.done_a + ng;
+  if (p->prec == 1 && k7_supported(p->l1, p->l2) && std::getenv("TFFT_NO_K7") == nullptr)
+    return launch_k7(inverse != 0, p->l1, p->l2, a, p->num_sms, st);
   return launch_k4(p->prec, inverse != 0, p->l1, p->l2, a, p->num_sms, st);
 }
 

@@ -41,7 +41,8 @@ namespace tfft {
 
 // cuTensorMapEncodeTiled through cudaGetDriverEntryPoint (resolved once)
 static int k4_encode_2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t dim0, uint64_t dim1,
-                        uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+                        uint64_t stride1_bytes, uint32_t box0, uint32_t box1,
+                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -57,8 +58,8 @@ static int k4_encode_2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, ui
   const cuuint64_t strides[1] = {stride1_bytes};
   const cuuint32_t box[2] = {box0, box1};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(map, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
@@ -423,6 +424,351 @@ static int launch_k4_t(const K4Args& a, int num_sms, cudaStream_t st) {
 // production tile shapes: 16 elements x 128 consumer threads (2048-element
 // tiles) and two CTAs per SM, so one CTA's exchange barriers overlap the
 // other's radix arithmetic
+// ===========================================================================
+// K7: K4's schedule with warp-local columns (FP64, columns <= 512 points).
+//  * tau-fastest thread map + group-mode exchanges: with TPS <= 32 a column's
+//    threads are one warp, so every exchange is a __syncwarp -- no CTA or
+//    named barrier on the FFT path (K5's structure, which reaches 95-98%);
+//  * tiles land by 2-D TMA in [column block][row][BW columns] regions with the
+//    hardware swizzle matching the BW*16-byte rows (32/64/128 B), so the
+//    tau-fastest staging reads (8 consecutive rows of one column per bank
+//    phase) are conflict-free;
+//  * the ring holds Z' p-major (the canonical q + N1 p layout): pass-A stores
+//    leave straight from registers in TPS-long runs, pass-B tiles are 2-D TMA
+//    boxes of the ring;
+//  * pass-B outputs are staged in a swizzled [row k][column] buffer and leave
+//    by one set of 2-D TMA stores per tile (one consumer barrier pair per B
+//    tile).
+template <int LOGL, bool INV>
+struct K7Ph {
+  static constexpr int L = 1 << LOGL;
+  using F = Fft<double, L, 16, INV, false, -1, true>;
+  static constexpr int TPS = F::TPS;
+  static constexpr int NT = 128;
+  static constexpr int CB = NT / TPS;
+  static_assert(TPS <= 32 && CB * TPS == NT, "warp-local columns");
+  static constexpr int BW = CB < 8 ? CB : 8;  // columns per TMA box (<= 128 B rows)
+  static constexpr int MASK = BW == 8 ? 7 : (BW == 4 ? 3 : (BW == 2 ? 1 : 0));
+  static constexpr CUtensorMapSwizzle SWZ =
+      BW == 8 ? CU_TENSOR_MAP_SWIZZLE_128B
+              : (BW == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : (BW == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE));
+  static constexpr int BOXR = L < 256 ? L : 256;
+  static constexpr int NBOX = L / BOXR;
+  // element (row r, column c) of a staged tile, as placed by the swizzled TMA
+  static __device__ __forceinline__ int sidx(int r, int c) {
+    const int off = (r * BW + (c % BW)) * 16;
+    return (c / BW) * (L * BW) + ((off ^ (((off >> 7) & MASK) << 4)) >> 4);
+  }
+  static constexpr int SLOTQ = (F::NPAD + 7) / 8 * 8 + (TPS < 8 ? TPS : 0);
+  static constexpr int ELEMS = CB * SLOTQ;
+};
+
+template <int L1, int L2, bool INV>
+struct K7Cfg {
+  using PA = K7Ph<L1, INV>;
+  using PB = K7Ph<L2, INV>;
+  static constexpr int NT = 128;
+  static constexpr int TILE = NT * 16;
+  static constexpr int SLOTS = PA::ELEMS > PB::ELEMS ? PA::ELEMS : PB::ELEMS;
+  static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));
+  static constexpr int RR = 4;
+  // stage and y-staging first (1024-byte aligned for the 128-byte swizzle)
+  static constexpr int SMEM = (2 * TILE + SLOTS + TWE) * 16 + 16 + RR * 24 + 1024 + 256;
+};
+
+__device__ __forceinline__ void k7_tma_store(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+
+template <int L1, int L2, bool INV>
+__global__ void __launch_bounds__(192, 2)
+    k7_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmz,
+              const __grid_constant__ CUtensorMap tmy, K4Args a) {
+  using K = K7Cfg<L1, L2, INV>;
+  using PA = typename K::PA;
+  using PB = typename K::PB;
+  using CT = double2;
+  constexpr int NT = K::NT;
+  constexpr int N1 = 1 << L1, N2 = 1 << L2;
+  constexpr int64_t N = int64_t(N1) * N2;
+  constexpr int LO = (L1 + L2 + 1) / 2;
+  constexpr int ncbA = N2 / PA::CB;
+  constexpr int ncbB = N1 / PB::CB;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  CT* stage = reinterpret_cast<CT*>(smem);
+  CT* ystage = stage + K::TILE;
+  CT* slots = ystage + K::TILE;
+  CT* tws1 = slots + K::SLOTS;
+  CT* tws2 = L1 == L2 ? tws1 : tws1 + N1;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tws1 + K::TWE);
+  uint64_t* empty = full + 1;
+  uint64_t* done = empty + 1;
+  uint64_t* relfree = done + K::RR;
+  long long* tk = reinterpret_cast<long long*>(relfree + K::RR);
+  long long* rtk = tk + 1;
+
+  const int tid = threadIdx.x;
+  const int G = (int)a.group;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&empty[0], NT / 32);
+    for (int i = 0; i < K::RR; ++i) {
+      mbar_init(&done[i], NT / 32);
+      mbar_init(&relfree[i], 1);
+    }
+    fence_mbar_init();
+  }
+  PA::F::build_pass_tables(tws1, static_cast<const CT*>(a.tw1), tid, NT + 64);
+  if constexpr (L1 != L2) PB::F::build_pass_tables(tws2, static_cast<const CT*>(a.tw2), tid, NT + 64);
+  __syncthreads();
+
+  if (tid >= NT + 32) {
+    // releaser (as K4)
+    if (tid != NT + 32) return;
+#pragma unroll 1
+    for (int it = 0;; ++it) {
+      const int i = it % K::RR;
+      mbar_wait_sleep(&done[i], (it / K::RR) & 1);
+      const long long t = rtk[i];
+      if (t < 0) return;
+      const K4Item c = k4_decode(a, t);
+      red_release_add(c.phase == 0 ? a.done_a + c.g : a.done_b + c.g, 1u);
+      mbar_arrive(&relfree[i]);
+    }
+  }
+  if (tid >= NT) {
+    // producer (as K4; both passes land by swizzled 2-D TMA boxes)
+    if (tid != NT) return;
+    long long t = (long long)atomicAdd(a.ticket, 1ull);
+    K4Item item = k4_decode(a, t);
+    long long t2 = (long long)atomicAdd(a.ticket, 1ull);
+    K4Item item2 = k4_decode(a, t2);
+#pragma unroll 1
+    for (int it = 0;; ++it) {
+      if (item.phase >= 0) {
+        while (!k4_ready(a, item)) __nanosleep(256);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      if (it >= 1) mbar_wait_sleep(&empty[0], (it & 1) ^ 1);
+      if (item.phase < 0) {
+        tk[0] = -1;
+        mbar_arrive(&full[0]);
+        return;
+      }
+      tk[0] = t;
+      const int r = (int)item.r;
+      mbar_expect_tx(&full[0], K::TILE * 16);
+      if (item.phase == 0) {
+        using P = PA;
+        const int sl = r / ncbA;
+        const int c0 = (r - sl * ncbA) * P::CB;
+        const int row0 = (int)((item.g * G + sl) * N1);
+#pragma unroll 1
+        for (int cb = 0; cb < P::CB / P::BW; ++cb)
+#pragma unroll 1
+          for (int b = 0; b < P::NBOX; ++b)
+            tma_load_2d(stage + cb * (N1 * P::BW) + b * P::BOXR * P::BW, &tmx, (c0 + cb * P::BW) * 2,
+                        row0 + b * P::BOXR, &full[0]);
+      } else {
+        using P = PB;
+        const int sl = r / ncbB;
+        const int q0 = (r - sl * ncbB) * P::CB;
+        const int row0 = (int)(((item.g % 3) * G + sl) * N2);
+#pragma unroll 1
+        for (int cb = 0; cb < P::CB / P::BW; ++cb)
+#pragma unroll 1
+          for (int b = 0; b < P::NBOX; ++b)
+            tma_load_2d(stage + cb * (N2 * P::BW) + b * P::BOXR * P::BW, &tmz, (q0 + cb * P::BW) * 2,
+                        row0 + b * P::BOXR, &full[0]);
+      }
+      t = t2;
+      item = item2;
+      if (item.phase >= 0) {
+        t2 = (long long)atomicAdd(a.ticket, 1ull);
+        item2 = k4_decode(a, t2);
+      }
+    }
+  }
+
+  // -------------------------------------------------------------- consumers
+  CT* __restrict__ z = static_cast<CT*>(a.z);
+  bool bad = false;
+#pragma unroll 1
+  for (int it = 0;; ++it) {
+    mbar_wait(&full[0], it & 1);
+    const long long t = tk[0];
+    const int ri = it % K::RR;
+    if (it >= K::RR) mbar_wait(&relfree[ri], ((it / K::RR) & 1) ^ 1);
+    if (tid == 0) rtk[ri] = t;
+    if (t < 0) {
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&done[ri]);
+      break;
+    }
+    const K4Item cur = k4_decode(a, t);
+    CT v[16];
+    const int r = (int)cur.r;
+    if (cur.phase == 0) {
+      using P = PA;
+      const int g = tid / P::TPS, tau = tid % P::TPS;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = stage[P::sidx(tau + P::TPS * k, g)];
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[0]);
+      const int sl = r / ncbA;
+      const int64_t sig = cur.g * G + sl;
+      const int p = (r - sl * ncbA) * P::CB + g;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) bad |= !finite2<double>(v[k]);
+      if (a.nfaults > 0) {
+        for (int f = 0; f < a.nfaults; ++f) {
+          const DevFault fl = a.faults[f];
+          if (fl.signal != sig || fl.stage != 0) continue;
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (p + (int64_t)(tau + P::TPS * k) * N2 == fl.element) {
+              if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
+              else v[k].y = flip_bits(v[k].y, fl.bit);
+            }
+        }
+      }
+      const CT* __restrict__ hi = static_cast<const CT*>(a.hi);
+      const CT* __restrict__ lo = static_cast<const CT*>(a.lo);
+      constexpr unsigned LOM = (1u << LO) - 1;
+      const unsigned mb = (unsigned)p * (unsigned)tau, ms = (unsigned)p * (unsigned)P::TPS;
+      const CT bh = __ldg(hi + (mb >> LO)), bl = __ldg(lo + (mb & LOM));
+      const CT sh = __ldg(hi + (ms >> LO)), sl_ = __ldg(lo + (ms & LOM));
+      P::F::run(slots + g * P::SLOTQ, v, tau, tws1, 2 + g);
+      CT* d = z + ((cur.g % 3) * G + sl) * N + (int64_t)p * N1;  // p-major ring
+      const CT step = cmul<double>(sh, sl_);
+      CT w = cmul<double>(bh, bl);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        constexpr int RL = P::F::RLAST;
+        const int k = (j % (16 / RL)) * RL + j / (16 / RL);
+        const int q = tau + P::TPS * j;
+        if (a.nfaults > 0 && a.strike_stage == 1) {
+          for (int f = 0; f < a.nfaults; ++f) {
+            const DevFault fl = a.faults[f];
+            if (fl.signal == sig && fl.stage == 1 && fl.element == q + (int64_t)p * N1) {
+              if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
+              else v[k].y = flip_bits(v[k].y, fl.bit);
+            }
+          }
+        }
+        d[q] = cmul<double>(v[k], w);
+        if (j + 1 < 16) w = cmul<double>(w, step);
+      }
+    } else {
+      using P = PB;
+      const int g = tid / P::TPS, tau = tid % P::TPS;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = stage[P::sidx(tau + P::TPS * k, g)];
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[0]);
+      {
+        // the tile's ring lines are dead: CB_B columns of N2 rows, 128-byte
+        // lines hold 8 columns, so only whole-line tiles (CB_B >= 8) discard
+        if constexpr (P::CB >= 8) {
+          const int sl = r / ncbB;
+          const int q0 = (r - sl * ncbB) * P::CB;
+          const CT* base = z + ((cur.g % 3) * G + sl) * N + q0;
+#pragma unroll 1
+          for (int i = tid; i < N2 * (P::CB / 8); i += NT)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (int64_t)(i / (P::CB / 8)) * N1 +
+                                                               (i % (P::CB / 8)) * 8)
+                         : "memory");
+        }
+      }
+      P::F::run(slots + g * P::SLOTQ, v, tau, tws2, 2 + g);
+      // outputs -> swizzled [k][column] staging -> 2-D TMA stores into y
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      fft_sync<NT>();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        CT val = v[k];
+        if constexpr (INV) val = cscale<double>(val, 1.0 / (double)N);
+        ystage[P::sidx(tau + P::TPS * P::F::out_pos(k), g)] = val;
+      }
+      fence_proxy_async();
+      fft_sync<NT>();
+      if (tid == 0) {
+        const int sl = r / ncbB;
+        const int q0 = (r - sl * ncbB) * P::CB;
+        const int row0 = (int)((cur.g * G + sl) * N2);
+#pragma unroll 1
+        for (int cb = 0; cb < P::CB / P::BW; ++cb)
+#pragma unroll 1
+          for (int b = 0; b < P::NBOX; ++b)
+            k7_tma_store(&tmy, ystage + cb * (N2 * P::BW) + b * P::BOXR * P::BW, (q0 + cb * P::BW) * 2,
+                         row0 + b * P::BOXR);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&done[ri]);
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
+}
+
+template <int L1, int L2, bool INV>
+static int launch_k7_t(const K4Args& a, int num_sms, cudaStream_t st) {
+  using K = K7Cfg<L1, L2, INV>;
+  auto kern = k7_kernel<L1, L2, INV>;
+  static bool configured = false;
+  static int per_sm = 1;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 192, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    if (per_sm < 1) per_sm = 1;
+    configured = true;
+  }
+  const int64_t total = (a.ngroups - 1) * (a.ta + a.tb) + a.ta_last + a.tb_last;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > total) grid = total;
+  if (grid < 1) return 0;
+  CUtensorMap tmx, tmz, tmy;
+  const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  // x: (B N1) rows of N2; ring: (3 G N2) rows of N1 (p-major); y: (B N2) rows of N1
+  int rc = k4_encode_2d(&tmx, dt, const_cast<void*>(a.x), (uint64_t)(2 << L2), (uint64_t)a.batch << L1,
+                        (uint64_t)16 << L2, (uint32_t)(2 * K::PA::BW), (uint32_t)K::PA::BOXR, K::PA::SWZ);
+  if (!rc)
+    rc = k4_encode_2d(&tmz, dt, a.z, (uint64_t)(2 << L1), (uint64_t)(3 * a.group) << L2, (uint64_t)16 << L1,
+                      (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
+  if (!rc)
+    rc = k4_encode_2d(&tmy, dt, a.y, (uint64_t)(2 << L1), (uint64_t)a.batch << L2, (uint64_t)16 << L1,
+                      (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
+  if (rc) return rc;
+  kern<<<(unsigned)grid, 192, K::SMEM, st>>>(tmx, tmz, tmy, a);
+  return (int)cudaGetLastError();
+}
+
+#define TFFT_K7_PAIRS TFFT_K4(7, 6) TFFT_K4(7, 7) TFFT_K4(8, 7) TFFT_K4(8, 8) TFFT_K4(8, 9) TFFT_K4(9, 9)
+
+bool k7_supported(int l1, int l2) {
+#define TFFT_K4(A, B) \
+  if (l1 == A && l2 == B) return true;
+  TFFT_K7_PAIRS
+#undef TFFT_K4
+  return false;
+}
+
+int launch_k7(bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
+#define TFFT_K4(A, B) \
+  if (l1 == A && l2 == B) return inverse ? launch_k7_t<A, B, true>(a, num_sms, st) : launch_k7_t<A, B, false>(a, num_sms, st);
+  TFFT_K7_PAIRS
+#undef TFFT_K4
+  return (int)cudaErrorInvalidValue;
+}
+
 // (FP32: 128-consumer CTAs measured faster up to 256-point columns, 256 beyond)
 template <typename T, int LMAX> struct K4Shape;
 template <int LMAX> struct K4Shape<double, LMAX> { static constexpr int E = 16, NT = 128, S = 1, MINB = 2; };

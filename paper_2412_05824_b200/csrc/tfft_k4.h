@@ -42,5 +42,9 @@ struct K4Args {
 bool k4_supported(int prec, int l1, int l2);
 int k4_columns_per_tile(int prec, int logl, int lmax);
 int launch_k4(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
+// K7: FP64 K4 variant with warp-local columns (columns <= 512 points); the
+// intermediate ring is p-major instead of K4's column-blocked layout
+bool k7_supported(int l1, int l2);
+int launch_k7(bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
 
 }  // namespace tfft
