@@ -277,8 +277,7 @@ def run_ours(args, dist):
         sweep.append({"n": n, "batch": b, "ms": round(t * 1e3, 4), "gflops": round(FLOP(n) * b / t / 1e9, 1),
                       "gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
                       "kernel": "k1_single_pass" if n <= 256 else ("k5_single_pass" if n <= 4096 else
-                                                                                   ("k7_fused_two_pass" if n <= 2 ** 18
-                                                                                    else "k4_fused_two_pass"))})
+                                                                                   "k7_fused_two_pass")})
     dom = max(range(len(sizes)), key=lambda i: statistics.mean(per_n[i]))
     dn = sweep[dom]
     roofline = {"bound": "hbm", "achieved": dn["gbs"], "peak": peak, "unit": "GB/s",

@@ -446,7 +446,7 @@ struct K7Ph {
   static constexpr int TPS = F::TPS;
   static constexpr int NT = 128;
   static constexpr int CB = NT / TPS;
-  static_assert(TPS <= 32 && CB * TPS == NT, "warp-local columns");
+  static_assert(TPS <= 64 && CB * TPS == NT, "warp-local columns (two warps at 1024 points)");
   static constexpr int BW = CB < 8 ? CB : 8;  // columns per TMA box (<= 128 B rows)
   static constexpr int MASK = BW == 8 ? 7 : (BW == 4 ? 3 : (BW == 2 ? 1 : 0));
   static constexpr CUtensorMapSwizzle SWZ =
@@ -472,8 +472,15 @@ struct K7Cfg {
   static constexpr int SLOTS = PA::ELEMS > PB::ELEMS ? PA::ELEMS : PB::ELEMS;
   static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));
   static constexpr int RR = 4;
-  // stage and y-staging first (1024-byte aligned for the 128-byte swizzle)
-  static constexpr int SMEM = (2 * TILE + SLOTS + TWE) * 16 + 16 + RR * 24 + 1024 + 256;
+  // stage first, then the column slots, both 1024-byte aligned for the
+  // 128-byte swizzle; pass-B outputs are staged in the slots (after the
+  // column FFTs are done), so no separate staging buffer is needed
+  // (1024-point columns only: at <= 512 points a separate staging buffer still
+  // fits two CTAs per SM and saves the wait for the stores' smem reads)
+  static constexpr bool ALIAS = L1 >= 10 || L2 >= 10;
+  static constexpr int SLOTS_AL = (SLOTS * 16 > TILE * 16 ? SLOTS : TILE);
+  static constexpr int SLOTS_SZ = (SLOTS_AL + 63) / 64 * 64;
+  static constexpr int SMEM = (TILE + (ALIAS ? 0 : TILE) + SLOTS_SZ + TWE) * 16 + 16 + RR * 24 + 1024 + 256;
 };
 
 __device__ __forceinline__ void k7_tma_store(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -501,9 +508,9 @@ __global__ void __launch_bounds__(192, 2)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   CT* stage = reinterpret_cast<CT*>(smem);
-  CT* ystage = stage + K::TILE;
-  CT* slots = ystage + K::TILE;
-  CT* tws1 = slots + K::SLOTS;
+  CT* slots = stage + K::TILE;
+  CT* ystage = K::ALIAS ? slots : slots + K::SLOTS_SZ;  // pass-B output staging
+  CT* tws1 = slots + K::SLOTS_SZ + (K::ALIAS ? 0 : K::TILE);
   CT* tws2 = L1 == L2 ? tws1 : tws1 + N1;
   uint64_t* full = reinterpret_cast<uint64_t*>(tws1 + K::TWE);
   uint64_t* empty = full + 1;
@@ -598,6 +605,7 @@ __global__ void __launch_bounds__(192, 2)
   // -------------------------------------------------------------- consumers
   CT* __restrict__ z = static_cast<CT*>(a.z);
   bool bad = false;
+  bool staged = false;  // the slots hold outputs a TMA store may still be reading
 #pragma unroll 1
   for (int it = 0;; ++it) {
     mbar_wait(&full[0], it & 1);
@@ -643,6 +651,11 @@ __global__ void __launch_bounds__(192, 2)
       const unsigned mb = (unsigned)p * (unsigned)tau, ms = (unsigned)p * (unsigned)P::TPS;
       const CT bh = __ldg(hi + (mb >> LO)), bl = __ldg(lo + (mb & LOM));
       const CT sh = __ldg(hi + (ms >> LO)), sl_ = __ldg(lo + (ms & LOM));
+      if (K::ALIAS && staged) {  // the previous B tile's TMA stores read the slots: wait, then reuse
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        fft_sync<NT>();
+        staged = false;
+      }
       P::F::run(slots + g * P::SLOTQ, v, tau, tws1, 2 + g);
       CT* d = z + ((cur.g % 3) * G + sl) * N + (int64_t)p * N1;  // p-major ring
       const CT step = cmul<double>(sh, sl_);
@@ -685,9 +698,15 @@ __global__ void __launch_bounds__(192, 2)
                          : "memory");
         }
       }
+      if (K::ALIAS && staged) {
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        fft_sync<NT>();
+        staged = false;
+      }
       P::F::run(slots + g * P::SLOTQ, v, tau, tws2, 2 + g);
-      // outputs -> swizzled [k][column] staging -> 2-D TMA stores into y
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      // outputs -> swizzled [k][column] staging (aliasing the slots: once every
+      // column's FFT is done) -> 2-D TMA stores into y
+      if (!K::ALIAS && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       fft_sync<NT>();
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
@@ -709,6 +728,7 @@ __global__ void __launch_bounds__(192, 2)
                          row0 + b * P::BOXR);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
+      staged = true;
     }
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&done[ri]);
@@ -751,7 +771,8 @@ static int launch_k7_t(const K4Args& a, int num_sms, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
-#define TFFT_K7_PAIRS TFFT_K4(7, 6) TFFT_K4(7, 7) TFFT_K4(8, 7) TFFT_K4(8, 8) TFFT_K4(8, 9) TFFT_K4(9, 9)
+#define TFFT_K7_PAIRS \
+  TFFT_K4(7, 6) TFFT_K4(7, 7) TFFT_K4(8, 7) TFFT_K4(8, 8) TFFT_K4(8, 9) TFFT_K4(9, 9) TFFT_K4(10, 9) TFFT_K4(10, 10)
 
 bool k7_supported(int l1, int l2) {
 #define TFFT_K4(A, B) \
