@@ -6,7 +6,7 @@ import csv, glob, json, os, re, sys
 src = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
 dst = sys.argv[2] if len(sys.argv) > 2 else "profiles/traffic.json"
 out = json.load(open(dst)) if os.path.exists(dst) else {}
-names = {"1m": 1 << 20}
+names = {"1m": 1 << 20, "256k": 1 << 18}
 for f in glob.glob(os.path.join(src, "prof_k*_fp64_n*.raw.csv")):
     m = re.search(r"prof_(k\d)_fp64_n(\w+)\.raw\.csv", f)
     if not m:
