@@ -340,6 +340,18 @@ int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, 
   return multipass(p, x, y, batch, inverse, st);
 }
 
+// protected sizes with a fused kernel: fused (checksums inside the transform)
+// or unfused (plain transform + one checksum sweep over x and y).
+// TFFT_ABFT_SWEEP=1 / =0 force either; the default is the measured-faster one.
+bool abft_use_sweep(const tfft_plan* p) {
+  if (const char* e = std::getenv("TFFT_ABFT_SWEEP")) return e[0] == '1';
+  // B200, 1 GiB inputs, T = 8 (tools/abft_ab.py): from 2^11 up the fused
+  // kernels lose to plain + sweep (FP32 4096: 1.03 vs 0.87 ms, FP64 4096:
+  // 1.44 vs 0.93 ms); below it the window sums of the sweep path (small
+  // windows: bs = 1 at 2^10) cost more than the fused kernel's occupancy loss
+  return p->logn >= 11;
+}
+
 }  // namespace
 
 extern "C" {
@@ -476,7 +488,8 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
   ab.nwin = nwin;
   // K5's fused ABFT (FP64 2^12 runs its inline-producer variant so the
   // window accumulators fit the register budget); K1 otherwise
-  const bool k5abft = p->k5 && p->logn >= 5 && p->logn <= 12 &&
+  const bool sweep = abft_use_sweep(p);
+  const bool k5abft = !sweep && p->k5 && p->logn >= 5 && p->logn <= 12 &&
                       std::getenv("TFFT_NO_K5_ABFT") == nullptr;
   if (k5abft) {
     int spt = 1, per_sm = 1;
@@ -510,7 +523,7 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     a.counters = (Counters*)counters;
     a.abft = ab;
     TFFT_TRY(launch_k5_abft(p->prec, p->logn, a, p->num_sms, st), "k5 abft launch");
-  } else if (p->k1) {
+  } else if (p->k1 && !sweep) {
     const int spt = k1_slots(p->prec, p->logn);
     if (W <= 4) {
       ab.mode = 0;

@@ -267,7 +267,7 @@ int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int
 
 // ---------------------------------------------------------------------------
 // one-sweep ABFT sums for the two-pass sizes: a CTA owns (window w, chunk of
-// CH = 256 * V = 1024 elements) and walks the window's signals once, reading x and y
+// CH = 256 * V = 1024 (FP32) / 512 (FP64) elements) and walks the window's signals once, reading x and y
 // exactly once per element. It accumulates the window sums s_in / s_out for
 // its chunk (working precision, as the reference's GEMV) and, per signal, the chunk's
 // partial c_in = row . x, ||x||^2 and c_out = e . y (working precision per
@@ -275,8 +275,8 @@ int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int
 // with no barrier in the signal loop; sweep_epilogue adds the partials in
 // (chunk, warp) order per signal.
 
-template <typename T, int V>
-__global__ void __launch_bounds__(256, 2) window_sweep_kernel(const C<T>* __restrict__ x, const C<T>* __restrict__ y,
+template <typename T, int V, int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) window_sweep_kernel(const C<T>* __restrict__ x, const C<T>* __restrict__ y,
                                                         int64_t n, int64_t batch, int64_t W, int64_t weight0,
                                                         const C<T>* __restrict__ row, const C<T>* __restrict__ tw,
                                                         int enc, C<T>* __restrict__ s_in, C<T>* __restrict__ s_out,
@@ -295,8 +295,9 @@ __global__ void __launch_bounds__(256, 2) window_sweep_kernel(const C<T>* __rest
     rw[i] = k < n ? row[k] : mk<T>(0, 0);
     ev[i] = k < n ? enc_value<T>(enc, k, n, tw) : mk<T>(0, 0);
   }
-  // loads of the next signal are issued before the current one is reduced
-  C<T> xv[V], yv[V];
+  // register ring of D signals: signal j's slot is refilled with j + D right
+  // after j is reduced, so D signals' loads are in flight per thread
+  C<T> xb[D][V], yb[D][V];
   auto load = [&](int64_t j, C<T>(&xa)[V], C<T>(&ya)[V]) {
 #pragma unroll
     for (int i = 0; i < V; ++i) {
@@ -305,36 +306,38 @@ __global__ void __launch_bounds__(256, 2) window_sweep_kernel(const C<T>* __rest
       ya[i] = (j < j1 && k < n) ? __ldcs(y + j * n + k) : mk<T>(0, 0);
     }
   };
-  load(j0, xv, yv);
+#pragma unroll
+  for (int d = 0; d < D; ++d) load(j0 + d, xb[d], yb[d]);
 #pragma unroll 1
-  for (int64_t j = j0; j < j1; ++j) {
-    C<T> xn[V], yn[V];
-    load(j + 1, xn, yn);
-    const T wj = (T)(weight0 + j + 1);
-    C<T> ci = mk<T>(0, 0), co = mk<T>(0, 0);
-    T fl = 0;
+  for (int64_t jb = j0; jb < j1; jb += D) {
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      ci = cadd<T>(ci, cmul<T>(rw[i], xv[i]));
-      fl = rfma(xv[i].x, xv[i].x, rfma(xv[i].y, xv[i].y, fl));
-      co = cadd<T>(co, cmul<T>(ev[i], yv[i]));
-      a_in[i] = mk<T>(rfma(wj, xv[i].x, a_in[i].x), rfma(wj, xv[i].y, a_in[i].y));
-      a_out[i] = mk<T>(rfma(wj, yv[i].x, a_out[i].x), rfma(wj, yv[i].y, a_out[i].y));
-    }
-    // warp partials: fixed xor tree in working precision (the products are
-    // working precision already), no CTA barrier inside the signal loop
-    T acc[5] = {ci.x, ci.y, fl, co.x, co.y};
+    for (int d = 0; d < D; ++d) {
+      const int64_t j = jb + d;
+      if (j < j1) {
+        const T wj = (T)(weight0 + j + 1);
+        C<T> ci = mk<T>(0, 0), co = mk<T>(0, 0);
+        T fl = 0;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1)
+        for (int i = 0; i < V; ++i) {
+          const C<T> xv = xb[d][i], yv = yb[d][i];
+          ci = cadd<T>(ci, cmul<T>(rw[i], xv));
+          fl = rfma(xv.x, xv.x, rfma(xv.y, xv.y, fl));
+          co = cadd<T>(co, cmul<T>(ev[i], yv));
+          a_in[i] = mk<T>(rfma(wj, xv.x, a_in[i].x), rfma(wj, xv.y, a_in[i].y));
+          a_out[i] = mk<T>(rfma(wj, yv.x, a_out[i].x), rfma(wj, yv.y, a_out[i].y));
+        }
+        // warp partials: fixed xor tree in working precision (the products are
+        // working precision already), no CTA barrier inside the signal loop
+        T acc[5] = {ci.x, ci.y, fl, co.x, co.y};
 #pragma unroll
-      for (int q = 0; q < 5; ++q) acc[q] = radd(acc[q], __shfl_xor_sync(0xffffffffu, acc[q], off));
-    if ((threadIdx.x & 31) == 0)
+        for (int off = 16; off >= 1; off >>= 1)
 #pragma unroll
-      for (int q = 0; q < 5; ++q) part[((j * nchunk + c) * 8 + (threadIdx.x >> 5)) * 5 + q] = (double)acc[q];
+          for (int q = 0; q < 5; ++q) acc[q] = radd(acc[q], __shfl_xor_sync(0xffffffffu, acc[q], off));
+        if ((threadIdx.x & 31) == 0)
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      xv[i] = xn[i];
-      yv[i] = yn[i];
+          for (int q = 0; q < 5; ++q) part[((j * nchunk + c) * 8 + (threadIdx.x >> 5)) * 5 + q] = (double)acc[q];
+      }
+      load(j + D, xb[d], yb[d]);
     }
   }
 #pragma unroll
@@ -385,15 +388,18 @@ int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64
                         const void* row, const void* tw, int enc, void* s_in, void* s_out, double* part,
                         const AbftArgs& ab, double delta, Counters* counters, cudaStream_t st) {
   const int64_t nwin = (batch + W - 1) / W;
-  const int64_t nchunk = prec == 0 ? (n + 2047) / 2048 : (n + 511) / 512;
+  // (V, D) = FP32 (4, 3), FP64 (2, 3): best of (8,1) (4,4) (2,6) / (1,6) (1,4)
+  // (2,4) on B200 (tools/abft_ab.py with the sweep route, 1 GiB, T = 8)
+  const int V = prec == 0 ? 4 : 2;
+  const int64_t nchunk = (n + 256 * V - 1) / (256 * V);
   const int64_t blocks = nwin * nchunk;
   if (blocks <= 0) return 0;
   if (prec == 0)
-    window_sweep_kernel<float, 8><<<(unsigned)blocks, 256, 0, st>>>(
+    window_sweep_kernel<float, 4, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(
         (const float2*)x, (const float2*)y, n, batch, W, weight0, (const float2*)row, (const float2*)tw, enc,
         (float2*)s_in, (float2*)s_out, part);
   else
-    window_sweep_kernel<double, 2><<<(unsigned)blocks, 256, 0, st>>>(
+    window_sweep_kernel<double, 2, 3, 2><<<(unsigned)blocks, 256, 0, st>>>(
         (const double2*)x, (const double2*)y, n, batch, W, weight0, (const double2*)row, (const double2*)tw, enc,
         (double2*)s_in, (double2*)s_out, part);
   int e = (int)cudaGetLastError();

@@ -12,7 +12,8 @@ tail -c 800 $OUT/bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-abft > /dev/null 2>&1
 sed -i 's/timeout 900 ncu/timeout 300 ncu/' tools/gpu_prof.sh
-bash tools/gpu_prof.sh "k4_fp64_n1m k4_kernel 1 1 --n 1048576 --prec double" "k4_fp64_n65536 k4_kernel 1 1 --n 65536 --prec double" \
-  "k5_fp64_n4096 k5_kernel 1 1 --n 4096 --prec double" "k5_fp64_n1024 k5_kernel 1 1 --n 1024 --prec double" \
-  "k5_fp32_n1024 k5_kernel 1 1 --n 1024 --prec single" "k5abft_fp32_n4096 k5_kernel 1 1 --n 4096 --prec single --abft" \
-  "k1_fp64_n256 k1_kernel 1 1 --n 256 --prec double" "k7_fp64_n65536 k7_kernel 1 1 --n 65536 --prec double" "k7_fp64_n1m k7_kernel 1 1 --n 1048576 --prec double"
+bash tools/gpu_prof.sh "k7_fp64_n1m k7_kernel 1 1 --n 1048576 --prec double" "k7_fp64_n65536 k7_kernel 1 1 --n 65536 --prec double" \
+  "k7_fp64_n256k k7_kernel 1 1 --n 262144 --prec double" "k5_fp64_n4096 k5_kernel 1 1 --n 4096 --prec double" \
+  "k5_fp64_n1024 k5_kernel 1 1 --n 1024 --prec double" "k5_fp32_n1024 k5_kernel 1 1 --n 1024 --prec single" \
+  "k1_fp64_n256 k1_kernel 1 1 --n 256 --prec double" "sweep_fp32_n4096 window_sweep 1 1 --n 4096 --prec single --abft" \
+  "sweep_fp64_n4096 window_sweep 1 1 --n 4096 --prec double --abft"
