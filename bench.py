@@ -372,7 +372,7 @@ def abft_overheads(args, dist):
                      "fused_ms": round(tfz * 1e3, 4), "overhead_pct": round(100 * (tfz / tp - 1), 2),
                      "plain_gbs": round(gbs, 1),
                      "path": "K5 transform + one-sweep checksums (measured faster than the fused K5 from 2^11)"
-                             if n <= 4096 else "K7 transform + one-sweep checksums"}
+                             if n <= 4096 else ("K7" if prec == "double" else "K4") + " transform + one-sweep checksums"}
         del x, y, sums
         torch.cuda.empty_cache()
     return res
