@@ -16,7 +16,7 @@ def main():
     from paper_2412_05824_b200 import abft as A, fft_core
     for prec in ("single", "double"):
         dt, rdt, bpc = ((torch.complex64, torch.float32, 8) if prec == "single" else (torch.complex128, torch.float64, 16))
-        for logn in (9, 10, 11, 12, 13, 16):
+        for logn in [int(v) for v in os.environ.get("ABFT_AB_LOGN", "9,10,11,12,13,16").split(",")]:
             n = 1 << logn
             b = (1 << 30) // (n * bpc)
             x = torch.randn(b * n * 2, dtype=rdt, device="cuda").view(dt).view(b, n)
