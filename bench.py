@@ -78,7 +78,11 @@ class Dist:
             torch.cuda.set_device(self.local)
         if self.world > 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("nccl" if device_backend else "gloo")
+            if device_backend:  # eager NCCL communicator (its handle feeds tfft_allreduce_stats)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+                dist.barrier()
+            else:
+                dist.init_process_group("gloo")
             self.pg = dist
         return self
 
@@ -335,7 +339,7 @@ def abft_overheads(args, dist):
     import torch
 
     import paper_2412_05824_b200 as tf
-    from paper_2412_05824_b200 import abft as A, fft_core
+    from paper_2412_05824_b200 import _lib, abft as A, fft_core, shard
 
     res = {}
     cases = [("C3_fp32_n4096", 4096, 32768, "single", 8), ("C3_fp64_n4096", 4096, 16384, "double", 8),
@@ -352,30 +356,82 @@ def abft_overheads(args, dist):
         ctr = fft_core._Counters()
         delta = A.default_delta(prec)
         offset = dist.rank * b  # global signal indices of this shard (weights w_j = j + 1)
-        red = torch.zeros(4, dtype=torch.int64, device="cuda")
 
         def plain():
             fft_core.device_execute(plan, x, y)
 
+        comm = shard._nccl_comm(dist.pg, "cuda") if dist.pg is not None else None
+        lib = _lib.load()
+
         def fused():
             A.protected_device(plan, x, y, delta=delta, group_size=T, counters=ctr, sums=sums,
                                signal_offset=offset)
-            if dist.pg is not None:  # K7: the only collective — fault counters over NVLink
-                red.copy_(ctr.dev)
-                dist.pg.all_reduce(red)
+            if comm is not None:
+                # the only collective: the triggered-signal count (int64 SUM) and
+                # the max divergence (its non-negative double bits, MAX) over
+                # NVLink, in one grouped NCCL launch on this stream
+                d = ctr.dev
+                rc = lib.tfft_allreduce_stats(d.data_ptr() + 8, 1, d.data_ptr() + 16, comm,
+                                              torch.cuda.current_stream().cuda_stream)
+                _lib.check(rc, "tfft_allreduce_stats")
 
         steps = max(args.steps, 5)
         tp = _time_loop(plain, steps, args.warmup, dist)
         tfz = _time_loop(fused, steps, args.warmup, dist)
         gbs = 2 * n * b * (8 if prec == "single" else 16) / tp / 1e9
+        api = None
+        if name.startswith("C5"):
+            api = c5_public_api(plan, x, b, T, dist, steps, args.warmup)
         res[name] = {"n": n, "batch_per_gpu": b, "T": T, "bs": plan.bs, "plain_ms": round(tp * 1e3, 4),
                      "fused_ms": round(tfz * 1e3, 4), "overhead_pct": round(100 * (tfz / tp - 1), 2),
                      "plain_gbs": round(gbs, 1),
                      "path": "K5 transform + one-sweep checksums (measured faster than the fused K5 from 2^11)"
                              if n <= 4096 else ("K7" if prec == "double" else "K4") + " transform + one-sweep checksums"}
+        if api is not None:
+            res[name]["public_api"] = api
         del x, y, sums
         torch.cuda.empty_cache()
     return res
+
+
+def c5_public_api(plan, x, b, T, dist, steps, warmup):
+    """C5 through the public sharded API (shard.run_protected_sharded on this
+    rank's device-resident shard of a world*b-signal batch): transform +
+    checksums + decisions + the counter all-reduce (NCCL C ABI when N > 1),
+    host synchronisation included. Wall clock per call, max over ranks."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2412_05824_b200 as tf
+    from paper_2412_05824_b200 import shard
+
+    world = dist.world
+    global_b = b * world
+    s0, s1, _ = shard.shard_bounds(global_b, plan.bs, T, world, dist.rank)
+    xs = x[: s1 - s0]
+    batch = tf.SignalBatch(xs)
+    pg = dist.pg if dist.pg is not None else None
+
+    def call():
+        if pg is None:
+            return tf.run_protected(plan, batch, group_size=T)
+        return shard.run_protected_sharded(plan, batch, global_b=global_b, rank=dist.rank, world=world, dist=tdist,
+                                           group_size=T, device="cuda", gather_reports=False)
+
+    for _ in range(warmup):
+        call()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    torch.cuda.synchronize()
+    el = dist.max((time.perf_counter() - t0) / steps)
+    return {"ms": round(el * 1e3, 4), "global_batch": global_b,
+            "call": "shard.run_protected_sharded(device shard, gather_reports=False)" if pg is not None
+            else "run_protected(device batch)",
+            "collective": "tfft_allreduce_stats (ncclAllReduce int64 SUM + f64 MAX, 48 B)" if pg is not None
+            else "none (1 GPU)"}
 
 
 def c1_config(args, dist):
@@ -485,7 +541,8 @@ def run_reference(args, dist):
     cb = cpu_reference(sizes, frac, workers, steps=args.steps, warmup=min(args.warmup, 1))
     return {
         "metric": "FFT GFLOP/s (5 N log2 N per transform), C2 FP64 sweep N=2^8..2^20",
-        "value": cb["value"], "unit": "GFLOP/s", "impl": "reference", "n_gpus": dist.world, "steps": args.steps,
+        "value": cb["value"], "unit": "GFLOP/s", "impl": "reference", "n_gpus": max(dist.world, args.gpus),
+        "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(cb["seconds"] * 1e3, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic (numpy normal)",
         "config": {"workload": "C2: FP64 complex 1-D forward FFT, N=2^8..2^20 (bounded CPU sample)",
@@ -495,8 +552,24 @@ def run_reference(args, dist):
     }
 
 
+def _spawn_ranks(args):
+    """``--gpus N`` without a torchrun environment: re-launch this script
+    under torch.distributed.run, one rank per GPU (rank 0 prints the line)."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return _spawn_ranks(args)
     dist = Dist()
     if args.impl == "reference":
         out = run_reference(args, dist)
@@ -504,6 +577,8 @@ def main():
             print(json.dumps(out), flush=True)
         return 0
     dist.init()
+    if dist.world != args.gpus and dist.rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={dist.world}; reporting {dist.world}", file=sys.stderr)
     out = run_ours(args, dist)
     if dist.rank == 0 and not args.no_cpu:
         out["cpu_baseline"] = cpu_reference(sweep_sizes(args.sweep), args.cpu_fraction, 1)

@@ -137,6 +137,17 @@ int tfft_row_checksums(tfft_plan* plan, const void* x, const void* y, int64_t ro
 int tfft_jou_variant(tfft_plan* plan, const void* x, void* out, int64_t rows, void* stream);
 int tfft_jou_undo(tfft_plan* plan, void* y, int64_t rows, void* stream);
 
+/* ---- multi-GPU (batch sharding) -------------------------- */
+
+/* The one collective of a sharded protected run: sums_dev[0..nsums) (int64:
+ * signal sweeps, verifications, corrections, recomputations, events) are
+ * SUM-reduced and max_dev[0] (max divergence, double) MAX-reduced across the
+ * ranks of `nccl_comm` (an ncclComm_t), in one ncclGroupStart/End on `stream`.
+ * NCCL comes from the libnccl.so.2 already loaded in the process (the one that
+ * made the communicator). Replaces the reference's single-process counters
+ * (abft.py:201-218, RunStats) for a batch split over GPUs. */
+int tfft_allreduce_stats(int64_t* sums_dev, int nsums, double* max_dev, void* nccl_comm, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

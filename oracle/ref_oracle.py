@@ -283,6 +283,21 @@ def roots(n, dtype, sign):
     return np.exp(1j * th).astype(dtype, copy=False)
 
 
+def gemv_checksum(e, n):
+    """dft_oracle.py:72-90: e^T W accumulated row by row (the cross-check order)."""
+    e = np.asarray(e)
+    if e.dtype not in (np.complex64, np.complex128):
+        e = e.astype(np.complex128)
+    if e.shape != (n,):
+        raise ValueError(f"encoding vector has length {e.shape}, expected ({n},)")
+    rt = roots(n, e.dtype, -1.0)
+    k = np.arange(n)
+    acc = np.zeros(n, dtype=e.dtype)
+    for j in range(n):
+        acc += e[j] * rt[(j * k) % n]
+    return acc
+
+
 def dft_naive(x):
     """dft_oracle.py:36-62 (forward), blocked O(N^2) direct sums."""
     x = np.asarray(x)

@@ -59,6 +59,7 @@ SIGNATURES = {
                                    c_int, c_vp]),
     "tfft_jou_variant": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "tfft_jou_undo": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "tfft_allreduce_stats": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp]),
 }
 
 _lib = None

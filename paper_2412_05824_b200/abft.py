@@ -536,8 +536,10 @@ def correct_pending(state: ChecksumState, outputs: SignalBatch, plan, enc, delta
 _FORCE_ENGINE = False
 
 
-def _prepare(plan, batch, e_left, delta):
-    """abft.py:627-645 (the non-finite check happens in-kernel)."""
+def _prepare(plan, batch, e_left, delta, sig_off=0, global_b=None):
+    """abft.py:627-645 (the non-finite check happens in-kernel). A shard of a
+    larger batch checks the single-precision weight limit on the GLOBAL
+    signal indices (its weights are sig_off + j + 1)."""
     _check_plan_batch(plan, batch, "forward")
     precision = batch.precision
     if delta is None:
@@ -545,7 +547,8 @@ def _prepare(plan, batch, e_left, delta):
     kind = e_left.kind if isinstance(e_left, EncodingVector) else e_left
     if kind not in LEFT_KINDS:
         raise ValueError(f"left encoding must be one of {LEFT_KINDS}, got {kind!r}")
-    if precision == "single" and batch.b > MAX_SINGLE_WEIGHT:  # sharded: checked on the global batch
+    top = max(sig_off + batch.b, global_b if global_b is not None else 0)
+    if precision == "single" and top > MAX_SINGLE_WEIGHT:
         raise ValueError("location weights above 2^24 are not exact in single precision")
     enc = e_left if isinstance(e_left, EncodingVector) else make_encoding_vector(kind, batch.n, precision)
     return precision, delta, kind, enc
@@ -583,7 +586,7 @@ def _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, ou
         raise ValueError("group size must be >= 1")
     if mode not in ("fused", "per-transaction"):
         raise ValueError(f"unknown mode {mode!r}")
-    precision, delta, kind, enc = _prepare(plan, batch, e_left, delta)
+    precision, delta, kind, enc = _prepare(plan, batch, e_left, delta, sig_off, global_b)
     stats = stats if stats is not None else RunStats()
     t = _device.require_cuda()
     x = _device.to_device(batch.data)

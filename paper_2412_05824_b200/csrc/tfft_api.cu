@@ -104,6 +104,11 @@ struct DevBuf {
 
 }  // namespace
 
+namespace tfft {
+// error reporting for the other C-ABI translation units (tfft_dist.cu)
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace tfft
+
 struct tfft_plan {
   int64_t n = 0;
   int logn = 0;
@@ -247,7 +252,10 @@ int strike_path(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse
 
 int zero_counters(tfft_plan* p, uint64_t*& counters, cudaStream_t st) {
   if (!counters) {
-    int e = p->counters.ensure(4 * sizeof(uint64_t));
+    // the plan's default counters are allocated once at their full size (8
+    // words: 4 for the caller-visible block, 4 for internal window FFTs), so a
+    // later ensure() never reallocates a buffer an earlier launch still uses
+    int e = p->counters.ensure(8 * sizeof(uint64_t));
     if (e) return cuda_fail(e, "counters");
     counters = (uint64_t*)p->counters.p;
   }
@@ -282,8 +290,12 @@ int upload_faults(tfft_plan* p, const std::vector<DevFault>& dev, cudaStream_t s
 
 // sizes beyond the fused kernels: the reference's own radix-4/2 pass list, one
 // device sweep per pass (correct for any N up to 2^29; not the fast path)
-int multipass(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, cudaStream_t st) {
+int multipass(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, uint64_t* counters,
+              cudaStream_t st) {
   const size_t cb = cbytes(p->prec);
+  // the fused kernels flag non-finite input while loading it; here one
+  // reduction over x sets the same counter (fft_core.py:305 raises on it)
+  if (counters) TFFT_TRY(launch_nonfinite(p->prec, x, batch * p->n, (Counters*)counters, st), "multipass finite check");
   int e = p->scratch_b.ensure((size_t)batch * p->n * cb);
   if (!e) e = p->base.ensure((size_t)p->n * cb);
   if (e) return cuda_fail(e, "multipass scratch");
@@ -302,15 +314,26 @@ int multipass(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, 
   return 0;
 }
 
-const void* enc_table(tfft_plan* p, bool inv) {
-  if (p->k1) return inv ? p->tw_inv.p : p->tw_fwd.p;
+// omega_N^k (conj for inv) for the Jou encoding of plans without K1's table;
+// built once, on the caller's stream (stream-ordered before every use on that
+// stream; no device-wide synchronisation, graph-capturable after first use)
+int enc_table(tfft_plan* p, bool inv, cudaStream_t st, const void** out) {
+  if (p->k1) {
+    *out = inv ? p->tw_inv.p : p->tw_fwd.p;
+    return 0;
+  }
   DevBuf& b = p->enc_tab[inv ? 1 : 0];
   if (!b.p) {
-    if (b.ensure((size_t)p->n * cbytes(p->prec))) return nullptr;
-    launch_base_table(p->prec, p->n, 1, inv ? 1 : 0, b.p, 0);
-    cudaDeviceSynchronize();
+    int e = b.ensure((size_t)p->n * cbytes(p->prec));
+    if (e) return cuda_fail(e, "encoding table");
+    e = launch_base_table(p->prec, p->n, 1, inv ? 1 : 0, b.p, st);
+    if (e) {
+      b.release();
+      return cuda_fail(e, "encoding table launch");
+    }
   }
-  return b.p;
+  *out = b.p;
+  return 0;
 }
 
 int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, int64_t signal_offset,
@@ -337,12 +360,16 @@ int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, 
     g_launches.fetch_add(k3_launches(p->k3), std::memory_order_relaxed);
     return rc ? cuda_fail(rc, "k3 launch") : 0;
   }
-  return multipass(p, x, y, batch, inverse, st);
+  return multipass(p, x, y, batch, inverse, counters, st);
 }
 
 // protected sizes with a fused kernel: fused (checksums inside the transform)
 // or unfused (plain transform + one checksum sweep over x and y).
 // TFFT_ABFT_SWEEP=1 / =0 force either; the default is the measured-faster one.
+bool abft_force_sweep() {
+  const char* e = std::getenv("TFFT_ABFT_SWEEP");
+  return e && e[0] == '1';
+}
 bool abft_use_sweep(const tfft_plan* p) {
   if (const char* e = std::getenv("TFFT_ABFT_SWEEP")) return e[0] == '1';
   // B200, 1 GiB inputs, T = 8 (tools/abft_ab.py): from 2^11 up the fused
@@ -486,32 +513,27 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
   ab.win_div = sums->win_div;
   ab.win_signals = W;
   ab.nwin = nwin;
-  // K5's fused ABFT (FP64 2^12 runs its inline-producer variant so the
-  // window accumulators fit the register budget); K1 otherwise
-  const bool sweep = abft_use_sweep(p);
-  const bool k5abft = !sweep && p->k5 && p->logn >= 5 && p->logn <= 12 &&
-                      std::getenv("TFFT_NO_K5_ABFT") == nullptr;
+  // K5 with the window sums in tensor memory (N = 2^9..2^12/13), K1's fused
+  // kernel below that, the plain transform + one checksum sweep otherwise
+  const bool k5abft = p->k5 && k5_abft_supported(p->prec, p->logn) && std::getenv("TFFT_NO_K5_ABFT") == nullptr &&
+                      !abft_force_sweep();
+  const bool sweep = !k5abft && abft_use_sweep(p);
   if (k5abft) {
-    int spt = 1, per_sm = 1;
-    k5_shape(p->prec, p->logn, 1, &spt, &per_sm);
-    const int64_t grid = (int64_t)p->num_sms * per_sm;
-    // pieces of >= SPT signals, ~8 per CTA over the batch
-    int64_t pl = (batch + 8 * grid - 1) / (8 * grid);
-    pl = std::max<int64_t>(spt, (pl + spt - 1) / spt * spt);
-    ab.mode = 1;
-    ab.pieces = std::max<int64_t>(1, (W + pl - 1) / pl);
-    if (ab.pieces > 1) {
-      int e = p->ws.ensure((size_t)nwin * ab.pieces * 2 * p->n * cbytes(p->prec));
-      if (e) return cuda_fail(e, "abft workspace");
-      const size_t cnt_bytes = (size_t)nwin * sizeof(unsigned);
-      if (p->win_count.cap < cnt_bytes) {
-        e = p->win_count.ensure(cnt_bytes);
-        if (e) return cuda_fail(e, "window counters");
-        TFFT_TRY((int)cudaMemsetAsync(p->win_count.p, 0, p->win_count.cap, st), "window counter memset");
-      }
-      ab.ws = p->ws.p;
-      ab.win_count = (unsigned*)p->win_count.p;
-    }
+    int64_t grid = 0;
+    int spt = 1;
+    int e = k5_abft_layout(p->prec, p->logn, p->num_sms, batch, &grid, &spt);
+    if (e) return cuda_fail(e, "k5 abft layout");
+    const int64_t per_cta = (batch + grid - 1) / grid;
+    const int64_t maxseg = (per_cta + W - 1) / W + 1;
+    const size_t cb = cbytes(p->prec);
+    e = p->ws.ensure((size_t)grid * maxseg * spt * 2 * p->n * cb);
+    if (!e) e = p->wsum.ensure((size_t)3 * nwin * p->n * cb);
+    if (!e) e = p->part.ensure((size_t)nwin * ((p->n + 8191) / 8192) * 2 * sizeof(double));
+    if (!e) e = p->counters.ensure(8 * sizeof(uint64_t));
+    if (e) return cuda_fail(e, "abft workspace");
+    ab.mode = 2;
+    ab.pieces = maxseg;
+    ab.ws = p->ws.p;
     K1Args a{};
     a.x = x;
     a.y = y;
@@ -523,6 +545,16 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     a.counters = (Counters*)counters;
     a.abft = ab;
     TFFT_TRY(launch_k5_abft(p->prec, p->logn, a, p->num_sms, st), "k5 abft launch");
+    char* s_in = (char*)p->wsum.p;
+    char* s_out = s_in + (size_t)nwin * p->n * cb;
+    char* ref = s_out + (size_t)nwin * p->n * cb;
+    TFFT_TRY(launch_seg_combine(p->prec, p->ws.p, p->n, batch, W, grid, maxseg, spt, nwin, s_in, s_out, st),
+             "abft window sums");
+    std::vector<DevFault> none;
+    rc = run_plain(p, s_in, ref, nwin, 0, 0, none, (uint64_t*)p->counters.p + 4, st);
+    if (rc) return rc;
+    TFFT_TRY(launch_group_div_chunked(p->prec, ref, s_out, p->n, nwin, sums->win_div, (double*)p->part.p, st),
+             "window group div");
   } else if (p->k1 && !sweep) {
     const int spt = k1_slots(p->prec, p->logn);
     if (W <= 4) {
@@ -572,7 +604,10 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     char* s_in = (char*)p->wsum.p;
     char* s_out = s_in + (size_t)nwin * p->n * cb;
     char* ref = s_out + (size_t)nwin * p->n * cb;
-    TFFT_TRY(launch_window_sweep(p->prec, x, y, p->n, batch, W, signal_offset, p->rows[enc].p, enc_table(p, false),
+    const void* etab = nullptr;
+    rc = enc_table(p, false, st, &etab);
+    if (rc) return rc;
+    TFFT_TRY(launch_window_sweep(p->prec, x, y, p->n, batch, W, signal_offset, p->rows[enc].p, etab,
                                  enc, s_in, s_out, (double*)p->part.p, ab, delta, (Counters*)counters, st),
              "abft sweep");
     std::vector<DevFault> none;
@@ -592,10 +627,13 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
   rc = strike_path(p, x, y, batch, 0, signal_offset, slow, st, &touched);
   if (rc) return rc;
   const size_t cb = cbytes(p->prec);
+  const void* etab = nullptr;
+  rc = enc_table(p, false, st, &etab);
+  if (rc) return rc;
   for (size_t i = 0; i < touched.size(); i += 2) {
     const int64_t a = touched[i], b = touched[i + 1];
-    TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, a, b - a, p->rows[enc].p,
-                                  p->k1 ? p->tw_fwd.p : enc_table(p, false), enc, delta, ab, (Counters*)counters, 1, st),
+    TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, a, b - a, p->rows[enc].p, etab, enc, delta, ab,
+                                  (Counters*)counters, 1, st),
              "strike row checksums");
     const int64_t w = a / W;
     const int64_t w0 = w * W, w1 = std::min<int64_t>(w0 + W, batch);
@@ -723,9 +761,10 @@ int tfft_correction_column(tfft_plan* p, const void* snap_in, const void* snap_o
 
 int tfft_patch_row(tfft_plan* p, void* y_row, const void* col, int enc, double* res_dev, void* stream) {
   if (!p) return fail(TFFT_EINVAL, "null plan");
-  TFFT_TRY(launch_patch_row(p->prec, y_row, col, p->n, enc, p->k1 ? p->tw_fwd.p : enc_table(p, false), res_dev,
-                            (cudaStream_t)stream),
-           "patch row");
+  const void* etab = nullptr;
+  int rc = enc_table(p, false, (cudaStream_t)stream, &etab);
+  if (rc) return rc;
+  TFFT_TRY(launch_patch_row(p->prec, y_row, col, p->n, enc, etab, res_dev, (cudaStream_t)stream), "patch row");
   return TFFT_OK;
 }
 
@@ -744,9 +783,11 @@ int tfft_row_checksums(tfft_plan* p, const void* x, const void* y, int64_t row0,
     if (e) return cuda_fail(e, "counters");
     counters = (uint64_t*)p->counters.p;
   }
-  TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, row0, nrows, p->rows[enc].p,
-                                p->k1 ? p->tw_fwd.p : enc_table(p, false), enc, delta, ab, (Counters*)counters, count,
-                                (cudaStream_t)stream),
+  const void* etab = nullptr;
+  rc = enc_table(p, false, (cudaStream_t)stream, &etab);
+  if (rc) return rc;
+  TFFT_TRY(launch_row_checksums(p->prec, x, y, p->n, row0, nrows, p->rows[enc].p, etab, enc, delta, ab,
+                                (Counters*)counters, count, (cudaStream_t)stream),
            "row checksums");
   return TFFT_OK;
 }
@@ -759,7 +800,9 @@ int tfft_jou_variant(tfft_plan* p, const void* x, void* out, int64_t rows, void*
 
 int tfft_jou_undo(tfft_plan* p, void* y, int64_t rows, void* stream) {
   if (!p) return fail(TFFT_EINVAL, "null plan");
-  const void* twi = p->k1 ? p->tw_inv.p : enc_table(p, true);
+  const void* twi = nullptr;
+  int rc = enc_table(p, true, (cudaStream_t)stream, &twi);
+  if (rc) return rc;
   TFFT_TRY(launch_jou(p->prec, 1, nullptr, y, rows, p->n, twi, (cudaStream_t)stream), "jou undo");
   return TFFT_OK;
 }

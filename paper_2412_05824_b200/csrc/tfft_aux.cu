@@ -137,6 +137,64 @@ int launch_scale(int prec, void* buf, int64_t count, double s, cudaStream_t st) 
   return (int)cudaGetLastError();
 }
 
+template <typename T>
+__global__ void nonfinite_kernel(const C<T>* __restrict__ buf, int64_t count, Counters* counters) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !finite2<T>(__ldcs(buf + i));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&counters->nonfinite, 1ull);
+}
+
+int launch_nonfinite(int prec, const void* buf, int64_t count, Counters* counters, cudaStream_t st) {
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (prec == 0) nonfinite_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float2*)buf, count, counters);
+  else nonfinite_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double2*)buf, count, counters);
+  return (int)cudaGetLastError();
+}
+
+// Window sums of the TMEM-fused K5 ABFT: window w's s_in / s_out = the sum of
+// the partials of every (CTA segment, slot) that covers part of it, added in
+// CTA then slot order (deterministic; tfft_k5.cu writes ws[(c*maxseg + j)*spt
+// + g][2][n] for CTA c's j-th segment).
+template <typename T>
+__global__ void seg_combine_kernel(const C<T>* __restrict__ ws, int64_t n, int64_t B, int64_t W, int64_t G,
+                                   int64_t maxseg, int spt, C<T>* __restrict__ s_in, C<T>* __restrict__ s_out) {
+  const int64_t w = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t w0 = w * W, w1 = min(w0 + W, B);
+  int64_t c = w0 * G / B;
+  while (c > 0 && c * B / G > w0) --c;
+  while (c < G && (c + 1) * B / G <= w0) ++c;
+  C<T> ai = mk<T>(0, 0), ao = mk<T>(0, 0);
+  for (; c < G; ++c) {
+    const int64_t lo = c * B / G, hi = (c + 1) * B / G;
+    if (lo >= w1) break;
+    if (hi <= lo) continue;
+    const int64_t j = w - lo / W;
+    for (int g = 0; g < spt; ++g) {
+      const C<T>* base = ws + ((c * maxseg + j) * spt + g) * 2 * n;
+      ai = cadd<T>(ai, base[i]);
+      ao = cadd<T>(ao, base[n + i]);
+    }
+  }
+  s_in[w * n + i] = ai;
+  s_out[w * n + i] = ao;
+}
+
+int launch_seg_combine(int prec, const void* ws, int64_t n, int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt,
+                       int64_t nwin, void* s_in, void* s_out, cudaStream_t st) {
+  const dim3 grid((unsigned)((n + 255) / 256), (unsigned)nwin);
+  if (prec == 0)
+    seg_combine_kernel<float><<<grid, 256, 0, st>>>((const float2*)ws, n, B, W, G, maxseg, spt, (float2*)s_in,
+                                                     (float2*)s_out);
+  else
+    seg_combine_kernel<double><<<grid, 256, 0, st>>>((const double2*)ws, n, B, W, G, maxseg, spt, (double2*)s_in,
+                                                      (double2*)s_out);
+  return (int)cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // block-wide deterministic FP64 sum (fixed tree), 256 threads
 

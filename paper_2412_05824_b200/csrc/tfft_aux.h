@@ -12,6 +12,8 @@ int launch_stockham_pass(int prec, const void* src, void* dst, int64_t rows, int
                          const void* base, int64_t base_stride, int inverse, cudaStream_t st);
 int launch_flip(int prec, void* buf, int64_t index, int part, int bit, cudaStream_t st);
 int launch_scale(int prec, void* buf, int64_t count, double s, cudaStream_t st);
+// counters->nonfinite |= any element of buf[0, count) (complex) is not finite
+int launch_nonfinite(int prec, const void* buf, int64_t count, Counters* counters, cudaStream_t st);
 int launch_row_checksums(int prec, const void* x, const void* y, int64_t n, int64_t row0, int64_t nrows,
                          const void* row, const void* tw, int enc, double delta, const AbftArgs& ab, Counters* counters,
                          int count, cudaStream_t st);
@@ -22,6 +24,9 @@ int64_t window_sweep_chunks(int64_t n);
 int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64_t batch, int64_t W, int64_t weight0,
                         const void* row, const void* tw, int enc, void* s_in, void* s_out, double* part,
                         const AbftArgs& ab, double delta, Counters* counters, cudaStream_t st);
+// window sums from the fused K5's per-(CTA segment, slot) partials
+int launch_seg_combine(int prec, const void* ws, int64_t n, int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt,
+                       int64_t nwin, void* s_in, void* s_out, cudaStream_t st);
 // group divergence of `count` long rows through chunk partials (part: count * ceil(n / 8192) * 2 doubles)
 int launch_group_div_chunked(int prec, const void* ref, const void* s_out, int64_t n, int64_t count, double* out,
                              double* part, cudaStream_t st);

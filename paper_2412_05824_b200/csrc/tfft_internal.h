@@ -39,9 +39,9 @@ struct AbftArgs {
   double* win_div;          // [nwin] group divergence of each verification window
   int64_t win_signals;      // W = T * bs signals per window (last may be short)
   int64_t nwin;
-  int mode;                 // 0: one window per slot (small W); 1: windows split into pieces
-  int64_t pieces;           // pieces per window (mode 1)
-  void* ws;                 // [nwin*pieces][2][N] working-precision partials (mode 1, pieces > 1)
+  int mode;                 // K1: 0 one window per slot (small W); 1 windows split into pieces
+  int64_t pieces;           // K1: pieces per window (mode 1); K5: segments per CTA
+  void* ws;                 // K1: [nwin*pieces][2][N]; K5: [grid][pieces][SPT][2][N] partial window sums
   unsigned int* win_count;  // [nwin] arrival counters (mode 1, pieces > 1), zero on entry
 };
 
@@ -62,13 +62,31 @@ int launch_k1(int prec, int logn, bool inverse, bool abft, const K1Args& a, int 
 int k1_supported(int prec, int logn);
 // K5: warp-specialised single-pass kernel (same sizes and results as K1's plain path)
 int launch_k5(int prec, int logn, bool inverse, const K1Args& a, int num_sms, cudaStream_t st);
-// K5 with the fused two-sided ABFT (forward only); a.abft.pieces = pieces per window
+// K5 with the fused two-sided ABFT (forward, N = 2^9..2^12 FP64 / 2^13 FP32):
+// window sums in tensor memory, per-(CTA segment, slot) partials written to
+// a.abft.ws ([grid][pieces][SPT][2][N], pieces = segments per CTA)
+int k5_abft_supported(int prec, int logn);
 int launch_k5_abft(int prec, int logn, const K1Args& a, int num_sms, cudaStream_t st);
-// signals per tile and CTAs per SM of a K5 instantiation (host-side work split)
-void k5_shape(int prec, int logn, int abft, int* spt, int* ctas_per_sm);
+// the grid and signals per tile the fused-ABFT launch will use for `batch`
+int k5_abft_layout(int prec, int logn, int num_sms, int64_t batch, int64_t* grid, int* spt);
 
 }  // namespace tfft
 
 namespace tfft {
 int k1_slots(int prec, int logn);
+
+// Per-device launch configuration cache: cudaFuncSetAttribute and the
+// occupancy query are per device, so a launcher's "configured" state is kept
+// per device ordinal (a function-static flag set on device 0 would
+// skip the attribute on device k).
+constexpr int kMaxDevices = 64;
+struct LaunchCfg {
+  bool done[kMaxDevices] = {};
+  int per_sm[kMaxDevices] = {};
+};
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : (d >= kMaxDevices ? kMaxDevices - 1 : d);
+}
 }

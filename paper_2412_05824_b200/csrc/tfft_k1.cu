@@ -467,11 +467,12 @@ template <typename T, int LOGN, bool INV, bool ABFT, int V>
 static int launch_one(const K1Args& a, int num_sms, cudaStream_t st) {
   using K = K1<T, LOGN, INV, ABFT, V>;
   auto kern = k1_kernel<T, LOGN, INV, ABFT, V>;
-  static bool configured = false;
-  if (!configured) {
+  static LaunchCfg cfg;
+  const int dev = current_device();
+  if (!cfg.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    configured = true;
+    cfg.done[dev] = true;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM);

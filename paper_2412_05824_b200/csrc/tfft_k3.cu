@@ -189,11 +189,12 @@ template <typename T, int LOGL, bool INV, int MODE>
 static int launch_col(const ColArgs& a, int num_sms, cudaStream_t st) {
   using K = ColCfg<T, LOGL>;
   auto kern = col_kernel<T, LOGL, INV, MODE>;
-  static bool configured = false;
-  if (!configured) {
+  static LaunchCfg cfg;
+  const int dev = current_device();
+  if (!cfg.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    configured = true;
+    cfg.done[dev] = true;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NT, K::SMEM);

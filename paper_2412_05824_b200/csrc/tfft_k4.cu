@@ -396,16 +396,18 @@ template <typename T, int L1, int L2, bool INV, int E, int NT, int S, int MINB>
 static int launch_k4_t(const K4Args& a, int num_sms, cudaStream_t st) {
   using K = K4Cfg<T, L1, L2, INV, E, NT, S>;
   auto kern = k4_kernel<T, L1, L2, INV, E, NT, S, MINB>;
-  static bool configured = false;
-  static int per_sm = 1;
-  if (!configured) {
+  static LaunchCfg cfg;
+  const int dev = current_device();
+  if (!cfg.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT + 64, K::SMEM);
+    int ps = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, NT + 64, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    if (per_sm < 1) per_sm = 1;
-    configured = true;
+    cfg.per_sm[dev] = ps < 1 ? 1 : ps;
+    cfg.done[dev] = true;
   }
+  const int per_sm = cfg.per_sm[dev];
   const int64_t total = (a.ngroups - 1) * (a.ta + a.tb) + a.ta_last + a.tb_last;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > total) grid = total;
@@ -741,16 +743,18 @@ template <int L1, int L2, bool INV>
 static int launch_k7_t(const K4Args& a, int num_sms, cudaStream_t st) {
   using K = K7Cfg<L1, L2, INV>;
   auto kern = k7_kernel<L1, L2, INV>;
-  static bool configured = false;
-  static int per_sm = 1;
-  if (!configured) {
+  static LaunchCfg cfg;
+  const int dev = current_device();
+  if (!cfg.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 192, K::SMEM);
+    int ps = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 192, K::SMEM);
     if (e != cudaSuccess) return (int)e;
-    if (per_sm < 1) per_sm = 1;
-    configured = true;
+    cfg.per_sm[dev] = ps < 1 ? 1 : ps;
+    cfg.done[dev] = true;
   }
+  const int per_sm = cfg.per_sm[dev];
   const int64_t total = (a.ngroups - 1) * (a.ta + a.tb) + a.ta_last + a.tb_last;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > total) grid = total;

@@ -79,3 +79,12 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+# -- the reference conftest's helpers (reference tests/conftest.py), used by the
+# vendored reference suite in tests/refsuite/ through ``from conftest import``
+
+
+def gaussian_batch(n, b, precision, seed=0):
+    from paper_2412_05824_b200 import SignalBatch
+    return SignalBatch(gaussian(n, b, precision, seed))

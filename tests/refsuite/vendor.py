@@ -1,0 +1,26 @@
+"""Copy the reference package's own test modules here, unmodified.
+
+    python tests/refsuite/vendor.py      # run HERE, where /root/reference exists
+
+VERDICT r1 (next #6) asks for the strongest drop-in proof: the reference's
+own suite (resilient-fft 0.1.0, /root/reference/pkg/tests) run against this
+package on the GPU. These files are TEST INFRASTRUCTURE, not product code:
+``tests/refsuite/conftest.py`` aliases ``resilient_fft`` to
+``paper_2412_05824_b200`` (and ``resilient_fft.dft_oracle`` to the oracle's
+O(N^2) DFT), and ``tests/conftest.py`` provides the reference conftest's
+helpers (gaussian_batch, oracle_tol, max_rel_error). The copies are committed
+because the GPU box has no /root/reference.
+"""
+
+import shutil
+from pathlib import Path
+
+SRC = Path("/root/reference/pkg/tests")
+DST = Path(__file__).resolve().parent
+FILES = ["test_backends.py", "test_fft_core.py", "test_abft.py", "test_fault.py", "test_plan.py",
+         "test_acceptance.py"]
+
+if __name__ == "__main__":
+    for f in FILES:
+        shutil.copyfile(SRC / f, DST / f)
+        print("vendored", f)

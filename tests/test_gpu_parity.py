@@ -190,7 +190,7 @@ def test_stockham_pass_boundary_and_butterflies():
 
 
 @pytest.mark.parametrize("precision", ["single", "double"])
-@pytest.mark.parametrize("log2n", [13, 14, 15, 16, 17, 18, 20])
+@pytest.mark.parametrize("log2n", [13, 14, 15, 16, 17, 18, 19, 20])
 def test_two_pass_sizes_vs_oracle(precision, log2n):
     """C2-style sizes through K3 (two-pass) against the oracle, both directions."""
     tf = _tf()
@@ -222,7 +222,9 @@ def test_multipass_beyond_two_pass(precision):
 
 
 @pytest.mark.parametrize("precision,log2n,groups", [("single", 14, 5), ("double", 16, 6), ("single", 20, 7),
-                                                   ("double", 13, 4), ("double", 17, 5)])
+                                                   ("double", 13, 4), ("double", 17, 5), ("double", 18, 5),
+                                                   ("double", 19, 5), ("double", 20, 5), ("single", 19, 5),
+                                                   ("single", 21, 4), ("single", 22, 3)])
 def test_fused_two_pass_many_groups(precision, log2n, groups):
     """K4 (fused two-pass, L2 intermediate ring): batches spanning several
     ring cycles plus a short last group, against numpy's FFT in FP64, and

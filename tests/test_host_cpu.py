@@ -170,3 +170,31 @@ def test_shard_bounds_whole_windows(b, bs, T, world):
         prev = e
     assert prev == b
     assert nwin_total == -(-(-(-b // bs)) // T)
+
+
+@pytest.mark.skipif(not LIB.exists(), reason="libtfft.so not built")
+def test_left_row_single_vs_reference_rows_at_scale():
+    """The FP32 wang rows the reference builds (abft.py:116-147: float32 roots
+    + BLAS GEMV for n <= 4096, its FP32 FFT above) vs the closed form here,
+    at n = 1024, 4096, 8192, 65536. Bitwise equality is impossible by
+    construction (BLAS summation order, a different FFT); what is pinned:
+    both agree to FP32 rounding, and the closed form is the more accurate of
+    the two against the FP64 row. Decision parity with these rows is checked
+    at C3/C5 scale by tests/test_gpu_scale.py (golden_scale.json)."""
+    rows = np.load(ROOT / "tests" / "golden" / "golden_scale_rows.npz")
+    lib = ctypes.CDLL(str(LIB))
+    for n in (1024, 4096, 8192, 65536):
+        ref32 = rows[f"wang_single_{n}"]
+        ref64 = rows[f"wang_double_{n}"]
+        out = np.empty(n, dtype=np.complex64)
+        assert lib.tfft_left_row(0, ctypes.c_int64(n), 0, out.ctypes.data_as(ctypes.c_void_p)) == 0
+        scale = np.abs(ref64).max()
+        d_ref = np.abs(ref32.astype(np.complex128) - ref64).max() / scale
+        d_ours = np.abs(out.astype(np.complex128) - ref64).max() / scale
+        d_both = np.abs(out.astype(np.complex128) - ref32.astype(np.complex128)).max() / scale
+        assert d_ours <= 1.0 * np.finfo(np.float32).eps, (n, d_ours)
+        assert d_ours <= d_ref, (n, d_ours, d_ref)
+        assert d_both <= 64 * np.finfo(np.float32).eps * np.log2(n), (n, d_both)
+        out64 = np.empty(n, dtype=np.complex128)
+        assert lib.tfft_left_row(0, ctypes.c_int64(n), 1, out64.ctypes.data_as(ctypes.c_void_p)) == 0
+        assert np.abs(out64 - ref64).max() <= 1e-13 * scale, n
