@@ -242,18 +242,32 @@ def _prec(plan):
 
 
 class _DeviceSums:
-    """Per-signal and per-window outputs of the fused kernel (tfft_sums)."""
+    """Per-signal and per-window outputs of the fused kernel (tfft_sums), and
+    the 4-word status block, carved from ONE device buffer laid out
+    [counters 4 | win_div nwin | c_in 2b | c_out 2b | floors b | div b] so a
+    clean run reads its status and window divergences in a single D2H copy."""
 
     def __init__(self, b, nwin):
-        self.c_in = _device.empty_f64(2 * b)
-        self.c_out = _device.empty_f64(2 * b)
-        self.floors = _device.empty_f64(b)
-        self.div = _device.empty_f64(b)
-        self.win_div = _device.empty_f64(max(nwin, 1))
+        t = _device.require_cuda()
+        nw = max(nwin, 1)
+        self.nwin = nw
+        self.buf = t.empty(4 + nw + 6 * b, dtype=t.float64, device="cuda")
+        o = 4 + nw
+        self.win_div = self.buf[4:o]
+        self.c_in = self.buf[o:o + 2 * b]
+        self.c_out = self.buf[o + 2 * b:o + 4 * b]
+        self.floors = self.buf[o + 4 * b:o + 5 * b]
+        self.div = self.buf[o + 5 * b:o + 6 * b]
+        self.counters = fft_core._Counters(self.buf[:4].view(t.int64))
 
     def struct(self):
         return _lib.TfftSums(self.c_in.data_ptr(), self.c_out.data_ptr(), self.floors.data_ptr(),
                              self.div.data_ptr(), self.win_div.data_ptr())
+
+    def status(self):
+        """(counters dict, win_div) in one device-to-host copy."""
+        h = self.buf[:4 + self.nwin].cpu().numpy()
+        return fft_core._Counters.decode(h[:4].view(np.int64)), h[4:]
 
     def host(self):
         c_in = self.c_in.cpu().numpy().view(np.complex128)
@@ -598,10 +612,9 @@ def _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, ou
     sums = _DeviceSums(batch.b, nwin)
     tx_off = sig_off // plan.bs
     faults = injector._collect(tx_off, tx_off + ntx) if injector is not None else []
-    counters = _Counters()
     protected_device(plan, source, y, kind=kind, delta=delta, group_size=group_size, faults=faults,
-                     counters=counters, sums=sums, signal_offset=sig_off)
-    c = counters.read()
+                     counters=sums.counters, sums=sums, signal_offset=sig_off)
+    c, win_div = sums.status()
     if c["nonfinite"]:
         for f in faults:
             f.fired = False
@@ -611,7 +624,6 @@ def _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, ou
         stats.signal_sweeps += 2 * batch.b  # unfused checksum reductions
     stats.max_divergence = max(stats.max_divergence, c["max_div"])
 
-    win_div = sums.win_div.cpu().numpy()
     if c["triggered"] == 0 and not _FORCE_ENGINE:
         reports = []
         for w in range(nwin):

@@ -117,11 +117,39 @@ def multi(name, n, b, precision, T, seed):
         inj.arm(rf.FaultSpec(**s), plan=plan, batch=batch)
     stats = rf.RunStats()
     t0 = time.time()
-    _, reports = rf.run_protected(plan, batch, group_size=T, injector=inj, stats=stats)
+    out, reports = rf.run_protected(plan, batch, group_size=T, injector=inj, stats=stats)
     rec = record(stats, reports)
+    rec["ref_err"] = repair_errors(plan, batch, out)
     print(f"  multi {name}: {len(specs)} faults, {len(stats.events)} events, {time.time() - t0:.1f}s", flush=True)
     return dict(name=name, n=n, b=b, precision=precision, T=T, seed=seed, spans=list(params.spans),
                 radices=list(params.radices), bs=params.bs, specs=specs, x_digest=digest(batch.data), result=rec)
+
+
+def repair_errors(plan, batch, out):
+    """Per-signal max |protected - clean| / max |clean| of the reference itself:
+    with several repaired faults in one run the FP32 correction residual can
+    exceed the single-fault bound of tests/test_acceptance.py:133-156."""
+    clean = rf.execute_plan(plan, batch).data
+    scale = np.maximum(np.abs(clean).max(axis=1), 1e-30)
+    return [float(v) for v in np.abs(out.data - clean).max(axis=1) / scale]
+
+
+def add_repair_errors():
+    """Augment an existing golden_scale.json with ``ref_err`` for the multi cases."""
+    path = HERE / "golden_scale.json"
+    payload = json.loads(path.read_text())
+    for case in payload["multi"]:
+        params = PlanParams(tuple(case["spans"]), tuple(case["radices"]), case["bs"])
+        plan = rf.build_plan(params, case["precision"])
+        batch = rfault._gaussian_batch(np.random.default_rng(case["seed"]), case["n"], case["b"], case["precision"])
+        assert digest(batch.data) == case["x_digest"]
+        inj = rf.FaultInjector(seu=False)
+        for s in case["specs"]:
+            inj.arm(rf.FaultSpec(**s), plan=plan, batch=batch)
+        out, _ = rf.run_protected(plan, batch, group_size=case["T"], injector=inj, stats=rf.RunStats())
+        case["result"]["ref_err"] = repair_errors(plan, batch, out)
+        print(f"  {case['name']}: max ref_err {max(case['result']['ref_err']):.3g}", flush=True)
+    path.write_text(json.dumps(payload, indent=0, default=float))
 
 
 def roc_full():
@@ -199,4 +227,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--repair-errors" in sys.argv:
+        add_repair_errors()
+    else:
+        main()

@@ -18,7 +18,7 @@ from conftest import gaussian
 
 pytestmark = pytest.mark.gpu
 
-SPEC = dict(transaction=21, signal=21, element=300, stage=0, part="re", bit=30)
+SPEC = dict(transaction=2, signal=70, element=300, stage=0, part="re", bit=30)
 N, B, T = 4096, 96, 2
 
 
