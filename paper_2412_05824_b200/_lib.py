@@ -76,7 +76,8 @@ def load(path=None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else Path(os.environ.get("TFFT_LIB", LIB_PATH))
+        # TFFT_LIB: an alternative build of the same C ABI (timing experiments, tools/)
+        p = Path(path) if path else Path(os.environ.get("TFFT_LIB") or LIB_PATH)
         if not p.exists():
             raise RuntimeError(
                 f"libtfft.so not found at {p}; build it with `python -c \"import __graft_entry__ as g; g.build()\"`"

@@ -67,7 +67,13 @@ class EncodingVector:
 
 
 def make_encoding_vector(kind, length, precision="double"):
-    """abft.py:80-104 (host metadata; the kernels evaluate the same vectors)."""
+    """abft.py:80-104 (host metadata; the kernels evaluate the same vectors).
+    The vector is read-only, so equal requests share one object."""
+    return _encoding_vector(kind, int(length), precision)
+
+
+@lru_cache(maxsize=32)
+def _encoding_vector(kind, length, precision):
     if length < 1:
         raise ValueError("length must be >= 1")
     if precision not in PRECISIONS:
@@ -606,8 +612,7 @@ def _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, ou
     x = _device.to_device(batch.data)
     source = _jou_variant_dev(plan, x) if kind == "jou" else x
     y = t.empty_like(x)
-    txs = transaction_partition(plan, batch)
-    ntx = len(txs)
+    ntx = (batch.b + plan.bs - 1) // plan.bs  # the Transaction objects only when the replay runs
     nwin = (ntx + group_size - 1) // group_size
     sums = _DeviceSums(batch.b, nwin)
     tx_off = sig_off // plan.bs
@@ -634,6 +639,7 @@ def _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, ou
     else:
         host = sums.host()
         run = _ProtectedRun(plan, source, y, delta, group_size, kind, stats, host, sig_off, global_b)
+        txs = transaction_partition(plan, batch)
         tx_by_index = {tx.index: tx for tx in txs}
         div = host[3]
         with np.errstate(over="ignore", invalid="ignore"):

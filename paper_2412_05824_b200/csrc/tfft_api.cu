@@ -136,6 +136,7 @@ struct tfft_plan {
   DevBuf counters;           // default counters
   DevBuf faults;
   DevBuf ws, win_count;
+  DevBuf sigpart;                     // K5 fused ABFT: per-warp per-signal partials
   DevBuf scratch_a, scratch_b, base;  // strike path
   DevBuf col_a, col_b, col64;         // single-column work
   K3Plan* k3 = nullptr;               // two-pass machinery (N beyond K1)
@@ -455,7 +456,7 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
 
 int tfft_plan_destroy(tfft_plan* p) {
   if (!p) return TFFT_OK;
-  DevBuf* all[] = {&p->part, &p->tw_fwd, &p->tw_inv, &p->enc_tab[0], &p->enc_tab[1], &p->wsum, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
+  DevBuf* all[] = {&p->sigpart, &p->part, &p->tw_fwd, &p->tw_inv, &p->enc_tab[0], &p->enc_tab[1], &p->wsum, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
                    &p->ws, &p->win_count, &p->scratch_a, &p->scratch_b, &p->base, &p->col_a, &p->col_b, &p->col64};
   for (DevBuf* b : all) b->release();
   if (p->k3) k3_destroy(p->k3);
@@ -520,20 +521,19 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
   const bool sweep = !k5abft && abft_use_sweep(p);
   if (k5abft) {
     int64_t grid = 0;
-    int spt = 1;
-    int e = k5_abft_layout(p->prec, p->logn, p->num_sms, batch, &grid, &spt);
+    int spt = 1, nws = 1;
+    int e = k5_abft_layout(p->prec, p->logn, p->num_sms, batch, &grid, &spt, &nws);
     if (e) return cuda_fail(e, "k5 abft layout");
     const int64_t per_cta = (batch + grid - 1) / grid;
     const int64_t maxseg = (per_cta + W - 1) / W + 1;
     const size_t cb = cbytes(p->prec);
     e = p->ws.ensure((size_t)grid * maxseg * spt * 2 * p->n * cb);
-    if (!e) e = p->wsum.ensure((size_t)3 * nwin * p->n * cb);
-    if (!e) e = p->part.ensure((size_t)nwin * ((p->n + 8191) / 8192) * 2 * sizeof(double));
-    if (!e) e = p->counters.ensure(8 * sizeof(uint64_t));
+    if (!e) e = p->sigpart.ensure((size_t)batch * nws * 5 * sizeof(double));
     if (e) return cuda_fail(e, "abft workspace");
     ab.mode = 2;
     ab.pieces = maxseg;
     ab.ws = p->ws.p;
+    ab.sig_part = (double*)p->sigpart.p;
     K1Args a{};
     a.x = x;
     a.y = y;
@@ -545,16 +545,9 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     a.counters = (Counters*)counters;
     a.abft = ab;
     TFFT_TRY(launch_k5_abft(p->prec, p->logn, a, p->num_sms, st), "k5 abft launch");
-    char* s_in = (char*)p->wsum.p;
-    char* s_out = s_in + (size_t)nwin * p->n * cb;
-    char* ref = s_out + (size_t)nwin * p->n * cb;
-    TFFT_TRY(launch_seg_combine(p->prec, p->ws.p, p->n, batch, W, grid, maxseg, spt, nwin, s_in, s_out, st),
-             "abft window sums");
-    std::vector<DevFault> none;
-    rc = run_plain(p, s_in, ref, nwin, 0, 0, none, (uint64_t*)p->counters.p + 4, st);
-    if (rc) return rc;
-    TFFT_TRY(launch_group_div_chunked(p->prec, ref, s_out, p->n, nwin, sums->win_div, (double*)p->part.p, st),
-             "window group div");
+    TFFT_TRY(launch_k5_window_finish(p->prec, p->logn, p->ws.p, (const double*)p->sigpart.p, nws, p->tw_fwd.p, batch,
+                                     W, grid, maxseg, spt, nwin, delta, ab, (Counters*)counters, p->num_sms, st),
+             "abft window finish");
   } else if (p->k1 && !sweep) {
     const int spt = k1_slots(p->prec, p->logn);
     if (W <= 4) {

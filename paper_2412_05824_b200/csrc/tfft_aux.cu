@@ -415,6 +415,7 @@ __global__ void sweep_epilogue_kernel(const double* __restrict__ part, int64_t n
                                       Counters* counters) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  double dmax = 0.0;  // one atomicMax per warp, not per signal
   for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < batch; r += nwarps) {
     double acc[5] = {0, 0, 0, 0, 0};
     for (int64_t i = lane; i < nparts; i += 32)
@@ -436,8 +437,19 @@ __global__ void sweep_epilogue_kernel(const double* __restrict__ part, int64_t n
     floors[r] = floor_v;
     div[r] = dv;
     if (dv > delta) atomicAdd(&counters->triggered, 1ull);
-    atomicMax(&counters->max_div_bits, (unsigned long long)__double_as_longlong(dv));
+    dmax = fmax(dmax, dv);
   }
+  if (lane == 0 && dmax > 0.0) atomicMax(&counters->max_div_bits, (unsigned long long)__double_as_longlong(dmax));
+}
+
+int launch_signal_epilogue(const double* part, int64_t nparts, int64_t n, int64_t batch, double delta,
+                           const AbftArgs& ab, Counters* counters, cudaStream_t st) {
+  int64_t eb = (batch + 7) / 8;
+  if (eb > 148 * 16) eb = 148 * 16;
+  if (eb < 1) return 0;
+  sweep_epilogue_kernel<<<(unsigned)eb, 256, 0, st>>>(part, nparts, n, batch, delta, ab.c_in, ab.c_out, ab.floors,
+                                                      ab.div, counters);
+  return (int)cudaGetLastError();
 }
 
 int64_t window_sweep_chunks(int64_t n) { return (n + 511) / 512; }  // upper bound (FP64 V = 2 -> 512 per chunk)

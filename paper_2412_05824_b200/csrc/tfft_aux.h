@@ -25,6 +25,10 @@ int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64
                         const void* row, const void* tw, int enc, void* s_in, void* s_out, double* part,
                         const AbftArgs& ab, double delta, Counters* counters, cudaStream_t st);
 // window sums from the fused K5's per-(CTA segment, slot) partials
+// per-signal c_in / c_out / floor / divergence from [batch][nparts][5] partials
+// (summed in a fixed order), counting triggers and the max divergence
+int launch_signal_epilogue(const double* part, int64_t nparts, int64_t n, int64_t batch, double delta,
+                           const AbftArgs& ab, Counters* counters, cudaStream_t st);
 int launch_seg_combine(int prec, const void* ws, int64_t n, int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt,
                        int64_t nwin, void* s_in, void* s_out, cudaStream_t st);
 // group divergence of `count` long rows through chunk partials (part: count * ceil(n / 8192) * 2 doubles)

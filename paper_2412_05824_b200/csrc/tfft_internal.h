@@ -43,6 +43,7 @@ struct AbftArgs {
   int64_t pieces;           // K1: pieces per window (mode 1); K5: segments per CTA
   void* ws;                 // K1: [nwin*pieces][2][N]; K5: [grid][pieces][SPT][2][N] partial window sums
   unsigned int* win_count;  // [nwin] arrival counters (mode 1, pieces > 1), zero on entry
+  double* sig_part;         // K5: [B][warps per signal][5] per-warp partials (c_in, ||x||^2, c_out)
 };
 
 struct K1Args {
@@ -68,7 +69,10 @@ int launch_k5(int prec, int logn, bool inverse, const K1Args& a, int num_sms, cu
 int k5_abft_supported(int prec, int logn);
 int launch_k5_abft(int prec, int logn, const K1Args& a, int num_sms, cudaStream_t st);
 // the grid and signals per tile the fused-ABFT launch will use for `batch`
-int k5_abft_layout(int prec, int logn, int num_sms, int64_t batch, int64_t* grid, int* spt);
+int k5_abft_layout(int prec, int logn, int num_sms, int64_t batch, int64_t* grid, int* spt, int* nws);
+int launch_k5_window_finish(int prec, int logn, const void* ws, const double* sig_part, int nws, const void* tw,
+                            int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta,
+                            const AbftArgs& ab, Counters* counters, int num_sms, cudaStream_t st);
 
 }  // namespace tfft
 

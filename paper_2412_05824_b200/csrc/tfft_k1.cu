@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT, V>::NT, K1<T, LOGN, INV
   }
   const CT* __restrict__ row = static_cast<const CT*>(a.abft.row);
   bool bad_input = false;
+  double dmax = 0.0;  // largest per-signal divergence this thread decided
 
   uint32_t it = 0;
 #pragma unroll 1
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT, V>::NT, K1<T, LOGN, INV
           a.abft.floors[sig] = floor_v;
           a.abft.div[sig] = dv;
           if (dv > a.abft.delta) atomicAdd(&a.counters->triggered, 1ull);
-          atomic_max_nonneg(&a.counters->max_div_bits, dv);
+          dmax = fmax(dmax, dv);
         }
       }
     }
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT, V>::NT, K1<T, LOGN, INV
     }
   }
   if (__any_sync(0xffffffffu, bad_input) && (tid & 31) == 0) atomicOr(&a.counters->nonfinite, 1ull);
+  if (ABFT && dmax > 0.0) atomic_max_nonneg(&a.counters->max_div_bits, dmax);  // once per thread, not per signal
 }
 
 // ---------------------------------------------------------------------------

@@ -17,9 +17,18 @@
 // Bitwise identical to K1 on every input: same passes, same twiddles, same
 // *_rn arithmetic.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "tfft_fft.cuh"
 #include "tfft_internal.h"
+
+#ifndef TFFT_K5_EXP
+#define TFFT_K5_EXP 0
+#endif
+#ifndef TFFT_K5_FP64_E4096
+#define TFFT_K5_FP64_E4096 16
+#endif
 
 namespace tfft {
 
@@ -30,7 +39,10 @@ struct K5 {
   // same radix schedule, ring and twiddle placement with and without ABFT: a
   // fault-free protected run must be bitwise equal to the plain transform
   // (tests/test_abft.py:197-206)
-  static constexpr int EMAX = 16;
+  // FP64 N = 4096 runs radix-8 (512 threads per signal, 17 warps per CTA):
+  // radix-16 legs need ~140 registers in FP64, so its 205 KB CTA could only
+  // run 9 warps per SM
+  static constexpr int EMAX = (sizeof(T) == 8 && LOGN >= 12) ? TFFT_K5_FP64_E4096 : 16;
   static constexpr int TPS0 = N / (EMAX < N ? EMAX : N);
   static constexpr int NT = TPS0 > 128 ? TPS0 : 128;  // consumer threads
   static constexpr int SLOT0 = N + (N >> 4);           // engine NPAD
@@ -50,12 +62,15 @@ struct K5 {
   static constexpr int SLOT = (F::NPAD + (16 / BPC) - 1) / (16 / BPC) * (16 / BPC);
   static constexpr int TILE = SPT * SLOT;
   static constexpr int TILE_BYTES = TILE * BPC;
-  // FP32 N = 4096 keeps two 288-thread CTAs per SM (<= 112 registers) with ABFT too
-  static constexpr int MINB = (NT <= 128 || (ABFT && sizeof(T) == 4 && NT == 256)) ? 2 : 1;
-  static constexpr int NTHR = NT + 32;
+  // FP32 N = 4096 / 8192: two CTAs per SM (<= 128 registers; ptxas chose 110
+  // without the bound, one CTA per SM, ncu occupancy 14%)
+  static constexpr int MINB = (NT <= 128 || (sizeof(T) == 4 && NT == 256)) ? 2 : 1;
+  // 256+ consumer threads: no producer warp (thread 0 refills a released
+  // slot), so a CTA is 8 (or 16) warps and two fit an SM's register file
+  static constexpr bool INL = NT >= 256;
+  static constexpr int NTHR = NT + (INL ? 0 : 32);
   static constexpr int NWARP_SLOT = TPS >= 32 ? TPS / 32 : 1;
-  // per-signal partials: 2 tile parities x SPT slots x warps x 5 doubles + arrival counters
-  static constexpr int RED_BYTES = ABFT ? (2 * SPT * NWARP_SLOT * 5 * 8 + 2 * SPT * 4 + 8) : 0;
+  static constexpr int RED_BYTES = 0;
   static constexpr int SMEM = S * TILE_BYTES + (TWS ? N * BPC : 0) + RED_BYTES + 2 * S * 8 + 64;
   // ---- ABFT accumulators in tensor memory: per consumer thread (its own TMEM
   // lane) three arrays of E complex values — s_in (window sum of w_j x_j at the
@@ -69,7 +84,7 @@ struct K5 {
   static constexpr int COLS_USED = BLK * NBLK;
   static constexpr int TCOLS = COLS_USED <= 32 ? 32 : COLS_USED <= 64 ? 64 : COLS_USED <= 128 ? 128
                              : COLS_USED <= 256 ? 256 : 512;
-  static_assert(!ABFT || (TPS >= 32 && E == 16 && NT % 128 == 0 && COLS_USED <= 512),
+  static_assert(!ABFT || (TPS >= 32 && E % (64 / BPC) == 0 && NT % 128 == 0 && COLS_USED <= 512),
                 "TMEM-fused ABFT needs whole-warp signals (N >= 512)");
 };
 
@@ -155,8 +170,7 @@ __device__ __forceinline__ void tmem_read(uint32_t taddr, C<T> (&v)[E]) {
 // g][2][N]; tfft_api.cu then adds a window's partials in (CTA, slot) order
 // (seg_combine_kernel), FFTs the window sums and forms the group divergence.
 template <typename T, int LOGN, bool INV, bool ABFT>
-__global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV, ABFT>::MINB)
-    k5_kernel(K1Args a) {
+__device__ __forceinline__ void k5_body(const K1Args& a) {
   using K = K5<T, LOGN, INV, ABFT>;
   using F = typename K::F;
   using CT = C<T>;
@@ -186,8 +200,6 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV,
   }
   if constexpr (ABFT) {
     if (tid < 32) tmem_alloc(tmem_base, K::TCOLS);
-    int* cnt = reinterpret_cast<int*>(red + 2 * SPT * K::NWARP_SLOT * 5);
-    for (int i = tid; i < 2 * SPT; i += K::NTHR) cnt[i] = 0;
     tmem_fence_before();
   }
   if constexpr (K::TWS) F::build_pass_tables(tws, static_cast<const CT*>(a.tw), tid, K::NTHR);
@@ -197,33 +209,58 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV,
 
   // tile sequence (identical in producer and consumers): plain = round robin;
   // ABFT = the segments of [lo, hi) in order, each in tiles of SPT signals
-  if (tid >= NT) {
+  struct Cursor {
+    int64_t t, ss, se;
+  };
+  auto first = [&]() {
+    Cursor c;
+    c.t = ABFT ? lo : (int64_t)blockIdx.x;
+    c.ss = lo;
+    c.se = ABFT ? min(hi, (lo / W + 1) * W) : 0;
+    return c;
+  };
+  auto next = [&](Cursor& c, int64_t& s0, int& nsig) -> bool {
+    if constexpr (!ABFT) {
+      if (c.t >= (B + SPT - 1) / SPT) return false;
+      s0 = c.t * SPT;
+      nsig = (int)min((int64_t)SPT, B - s0);
+      c.t += gridDim.x;
+    } else {
+      if (c.t >= c.se) {  // next segment (window piece) of [lo, hi)
+        c.ss = c.se;
+        if (c.ss >= hi) return false;
+        c.se = min(hi, (c.ss / W + 1) * W);
+        c.t = c.ss;
+      }
+      if (c.t >= hi) return false;
+      s0 = c.t;
+      nsig = (int)min((int64_t)SPT, c.se - s0);
+      c.t += SPT;
+    }
+    return true;
+  };
+  auto land = [&](int slot, int64_t s0, int nsig) {
+    CT* dst = ring + slot * K::TILE;
+    mbar_expect_tx(&full[slot], (uint32_t)(nsig * N * K::BPC));
+    for (int gg = 0; gg < nsig; ++gg) bulk_g2s(dst + gg * K::SLOT, x + (s0 + gg) * N, N * K::BPC, &full[slot]);
+  };
+  Cursor pc = first();  // producer cursor (producer warp, or thread 0 when inline)
+  if constexpr (K::INL) {
+    if (tid == 0) {
+      int64_t s0;
+      int nsig;
+      for (int i = 0; i < S && next(pc, s0, nsig); ++i) land(i, s0, nsig);
+    }
+  } else if (tid >= NT) {
     // ------------------------------------------------------------ producer
     if (tid != NT) return;
-    int it = 0;
-    auto land = [&](int64_t s0, int nsig) {
+    int64_t s0;
+    int nsig;
+#pragma unroll 1
+    for (int it = 0; next(pc, s0, nsig); ++it) {
       const int s = it % S;
       if (it >= S) mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
-      CT* dst = ring + s * K::TILE;
-      mbar_expect_tx(&full[s], (uint32_t)(nsig * N * K::BPC));
-      for (int gg = 0; gg < nsig; ++gg) bulk_g2s(dst + gg * K::SLOT, x + (s0 + gg) * N, N * K::BPC, &full[s]);
-      ++it;
-    };
-    if constexpr (!ABFT) {
-      const int64_t ntiles = (B + SPT - 1) / SPT;
-#pragma unroll 1
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t s0 = t * SPT;
-        land(s0, (int)min((int64_t)SPT, B - s0));
-      }
-    } else {
-#pragma unroll 1
-      for (int64_t ss = lo; ss < hi;) {
-        const int64_t se = min(hi, (ss / W + 1) * W);
-#pragma unroll 1
-        for (int64_t s0 = ss; s0 < se; s0 += SPT) land(s0, (int)min((int64_t)SPT, se - s0));
-        ss = se;
-      }
+      land(s, s0, nsig);
     }
     return;
   }
@@ -269,7 +306,12 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV,
         tmem_wait_st();
         const T w = (T)(a.weight0 + sig + 1);
         CT r[E];
+#if TFFT_K5_EXP & 1  // experiment: no TMEM traffic (timing only)
+#pragma unroll
+        for (int k = 0; k < E; ++k) r[k] = mk<T>((T)1, (T)0);
+#else
         tmem_read<T, E>(t_row, r);
+#endif
         T cr = 0, cim = 0, fl = 0;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
@@ -277,7 +319,9 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV,
           cim = rfma(r[k].x, v[k].y, rfma(r[k].y, v[k].x, cim));
           fl = rfma(v[k].x, v[k].x, rfma(v[k].y, v[k].y, fl));
         }
+#if !(TFFT_K5_EXP & 1)
         tmem_axpy<T, E>(t_sin, w, v);
+#endif
         red5[0] = (double)cr;
         red5[1] = (double)cim;
         red5[2] = (double)fl;
@@ -297,12 +341,22 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV,
           }
       }
     }
-    F::run(buf, v, tau, tw, 2 + g);
+    F::run(buf, v, tau, tw, SPT == 1 ? 2 : 2 + g);  // a constant id when one signal per tile (ptxas then reserves 3 barriers, not 16: 16 capped the fused entry at one CTA per SM)
     // this warp's reads of the slot are complete: hand it back to the
     // producer (generic-proxy writes ordered before the next bulk copy)
     fence_proxy_async();
     __syncwarp();
     if ((tid & 31) == 0) k5_arrive(&empty[s]);
+    if constexpr (K::INL) {
+      // inline producer: once every consumer warp has released this slot,
+      // thread 0 lands the tile S ahead into it
+      if (tid == 0) {
+        int64_t n0;
+        int nn;
+        mbar_wait(&empty[s], ((it - 1) / S) & 1);
+        if (next(pc, n0, nn)) land(s, n0, nn);
+      }
+    }
     if constexpr (INV) {
       const T sc = (T)(1.0 / (double)N);
 #pragma unroll
@@ -350,67 +404,35 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV,
             co = acc;
           }
         }
+#if !(TFFT_K5_EXP & 1)
         tmem_axpy<T, E>(t_sout, w, v);
+#endif
         red5[3] = (double)co.x;
         red5[4] = (double)co.y;
       }
-      // per-signal totals without a CTA barrier: xor-shuffle tree inside each
-      // warp (working precision); for TPS > 32 the slot's warps publish
-      // partials and the last one to arrive (shared-memory counter) adds them
-      // in warp order in FP64
-      constexpr int W0 = TPS < 32 ? TPS : 32;
+#if TFFT_K5_EXP & 2  // experiment: no per-signal reduction (timing only)
+      if (false) {
+#else
       {
+#endif
+        // per-signal totals are finished OUTSIDE this kernel: each warp
+        // reduces its lanes with a fixed xor tree (working precision) and
+        // lane 0 stores the warp's 5 partials; launch_signal_epilogue adds a
+        // signal's warps in order and decides it. No CTA barrier and no
+        // serial FP64 tail on the FFT warps' path (that tail cost +0.17 ms
+        // at C3 FP32).
+        constexpr int W0 = TPS < 32 ? TPS : 32;
+        constexpr int NWS = TPS >= 32 ? TPS / 32 : 1;
         T r5[5] = {(T)red5[0], (T)red5[1], (T)red5[2], (T)red5[3], (T)red5[4]};
 #pragma unroll
         for (int off = W0 / 2; off >= 1; off >>= 1)
 #pragma unroll
           for (int kk = 0; kk < 5; ++kk) r5[kk] = radd(r5[kk], __shfl_xor_sync(0xffffffffu, r5[kk], off));
+        if (valid && (tau & 31) == 0) {
+          double* dst = a.abft.sig_part + (sig * NWS + (tau >> 5)) * 5;
 #pragma unroll
-        for (int kk = 0; kk < 5; ++kk) red5[kk] = (double)r5[kk];
-      }
-      bool fin = valid && tau == 0;
-      if constexpr (TPS > 32) {
-        constexpr int NW = TPS / 32;
-        const int par = (it - 1) & 1;
-        double* rp = red + ((par * SPT + g) * NW) * 5;
-        fin = false;
-        if ((tau & 31) == 0) {
-#pragma unroll
-          for (int kk = 0; kk < 5; ++kk) rp[(tau >> 5) * 5 + kk] = red5[kk];
-          __threadfence_block();
-          int* cnt = reinterpret_cast<int*>(red + 2 * SPT * NW * 5) + par * SPT + g;
-          if (atomicAdd(cnt, 1) == NW - 1) {
-            __threadfence_block();
-#pragma unroll
-            for (int kk = 0; kk < 5; ++kk) {
-              double acc = rp[kk];
-              for (int i = 1; i < NW; ++i) acc += rp[i * 5 + kk];
-              red5[kk] = acc;
-            }
-            *cnt = 0;
-            fin = valid;
-          }
+          for (int kk = 0; kk < 5; ++kk) dst[kk] = (double)r5[kk];
         }
-      }
-      if (fin) {
-        const double cin_r = red5[0], cin_i = red5[1];
-        const double co_r = red5[3], co_i = red5[4];
-        const double floor_v = sqrt(red5[2]) / sqrt((double)N);
-        double dv;
-        if (!isfinite(co_r) || !isfinite(co_i)) {
-          dv = __longlong_as_double(0x7ff0000000000000ll);
-        } else {
-          const double den = fmax(fmax(hypot(cin_r, cin_i), floor_v), 1e-30);
-          dv = hypot(cin_r - co_r, cin_i - co_i) / den;
-        }
-        a.abft.c_in[2 * sig] = cin_r;
-        a.abft.c_in[2 * sig + 1] = cin_i;
-        a.abft.c_out[2 * sig] = co_r;
-        a.abft.c_out[2 * sig + 1] = co_i;
-        a.abft.floors[sig] = floor_v;
-        a.abft.div[sig] = dv;
-        if (dv > a.abft.delta) atomicAdd(&a.counters->triggered, 1ull);
-        atomicMax(&a.counters->max_div_bits, (unsigned long long)__double_as_longlong(dv));
       }
     }
   };
@@ -458,20 +480,63 @@ __global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV,
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
 }
 
+template <typename T, int LOGN, bool INV, bool ABFT>
+__global__ void __launch_bounds__(K5<T, LOGN, INV, ABFT>::NTHR, K5<T, LOGN, INV, ABFT>::MINB)
+    k5_kernel(K1Args a) {
+  k5_body<T, LOGN, INV, ABFT>(a);
+}
+
+// The fused-ABFT entry of the two-CTA-per-SM shapes (FP32 N = 4096 / 8192,
+// 256 threads): the occupancy calculator keeps one CTA per SM at 121-128
+// registers (the API reports no room for a second CTA above 112), so the register cap is explicit (__maxnreg__ cannot be combined
+// with __launch_bounds__, hence a separate entry)
+template <typename T, int LOGN, bool INV>
+__global__ void __maxnreg__(112) k5_abft2_kernel(K1Args a) {
+  k5_body<T, LOGN, INV, true>(a);
+}
+
+template <typename T, int LOGN, bool INV, bool ABFT>
+static auto k5_entry() {
+  using K = K5<T, LOGN, INV, ABFT>;
+  if constexpr (ABFT && K::MINB == 2 && K::INL) return k5_abft2_kernel<T, LOGN, INV>;
+  else return k5_kernel<T, LOGN, INV, ABFT>;
+}
+
 // configured grid of a K5 instantiation on the current device (the fused
 // ABFT's per-CTA signal ranges, and so its partial-sum layout, depend on it)
 template <typename T, int LOGN, bool INV, bool ABFT>
 static int k5_grid_t(int num_sms, int64_t batch, int64_t* grid_out) {
   using K = K5<T, LOGN, INV, ABFT>;
-  auto kern = k5_kernel<T, LOGN, INV, ABFT>;
+  auto kern = k5_entry<T, LOGN, INV, ABFT>();
   static LaunchCfg cfg;
   const int dev = current_device();
   if (!cfg.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
+    // the largest shared-memory carveout, so two ~100 KB CTAs can share an SM
+    // (the driver otherwise picked the 132 KB configuration: one CTA per SM)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return (int)e;
     int ps = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, K::NTHR, K::SMEM);
     if (e != cudaSuccess) return (int)e;
+    if (std::getenv("TFFT_DEBUG_OCC")) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      size_t avail = 0;
+      cudaOccupancyAvailableDynamicSMemPerBlock(&avail, kern, 2, K::NTHR);
+      std::fprintf(stderr, "k5<%d,%d,%d,%d> occupancy %d (smem %d, threads %d, tcols %d, regs %d, static %zu, "
+                   "local %zu, maxthr %d, avail_dyn@2 %zu)\n", (int)sizeof(T), LOGN, (int)INV, (int)ABFT, ps,
+                   K::SMEM, K::NTHR, ABFT ? K::TCOLS : 0, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes,
+                   fa.maxThreadsPerBlock, avail);
+    }
+    // The occupancy calculator answers 1 for the TMEM-allocating fused entry
+    // even at 112 registers (cudaOccupancyAvailableDynamicSMemPerBlock(2) =
+    // 0), but two of its CTAs (2 x 102 KB smem, 2 x 256 TMEM columns, 2 x 256
+    // threads x 112 registers) do run concurrently: forcing 296 CTAs took C3
+    // FP32 from 0.666 to 0.569 ms. CTAs never wait on each other here, so a
+    // grid the SM could not co-schedule would serialise, not deadlock.
+    if (ABFT && K::INL && K::MINB == 2) ps = 2;
     // ABFT: the TMEM columns of the CTAs sharing an SM must fit its 512
     if (ABFT) ps = std::min(ps, 512 / K::TCOLS);
     cfg.per_sm[dev] = ps < 1 ? 1 : ps;
@@ -490,7 +555,7 @@ static int launch_k5_t(const K1Args& a, int num_sms, cudaStream_t st) {
   int e = k5_grid_t<T, LOGN, INV, ABFT>(num_sms, a.batch, &grid);
   if (e) return e;
   if (grid < 1) return 0;
-  k5_kernel<T, LOGN, INV, ABFT><<<(unsigned)grid, K::NTHR, K::SMEM, st>>>(a);
+  k5_entry<T, LOGN, INV, ABFT>()<<<(unsigned)grid, K::NTHR, K::SMEM, st>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -520,13 +585,179 @@ int launch_k5(int prec, int logn, bool inverse, const K1Args& a, int num_sms, cu
 int k5_abft_supported(int prec, int logn) { return logn >= 9 && logn <= (prec == 0 ? 13 : 12); }
 
 // fused-ABFT instantiations: N = 2^9 .. 2^12 (FP64) / 2^13 (FP32); query = grid only
+// ---------------------------------------------------------------------------
+// Window finisher of the fused K5 route (abft.py:592-624 + :648-665), ONE
+// launch after the transform instead of five (per-signal epilogue, segment
+// combine, window FFT, group divergence): CTA w (grid-stride) owns window w.
+//   1. s_in / s_out of the window: the CTAs' segment partials added in (CTA,
+//      slot) order, s_in at this thread's pass-0 positions, s_out at its
+//      output positions;
+//   2. ref = FFT(s_in) in shared memory (the same engine, passes and twiddle
+//      values as the plain K5 transform, so ref equals run_plain's output);
+//   3. group_div = ||ref - s_out|| / max(||ref||, 1e-30) in FP64 (fixed trees);
+//   4. the window's signals: warp per signal, its warps' 5 partials added in
+//      order, then c_in / c_out / floor / divergence and the counters (one
+//      atomicMax per thread, not per signal).
+template <typename T, int LOGN>
+struct WinFin {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int TPS = N / 16;
+  static constexpr int NT = TPS < 256 ? 256 : TPS;
+  static constexpr int GW = NT / TPS;  // windows in flight per CTA (one per thread group)
+  // group mode: a window's TPS threads sync among themselves (named barrier
+  // 1 + g, or __syncwarp at TPS == 32)
+  using F = Fft<T, N, 16, false, false, -1, false>;
+  static constexpr int NW = TPS / 32;  // warps per window
+  static constexpr int SMEM = GW * F::NPAD * (int)sizeof(C<T>) + GW * NW * 2 * 8;
+  static_assert(TPS >= 32, "window finisher needs N >= 512");
+};
+
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(WinFin<T, LOGN>::NT) k5_window_finish(
+    const C<T>* __restrict__ ws, const double* __restrict__ sig_part, int nws, const C<T>* __restrict__ tw,
+    int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta, AbftArgs ab,
+    Counters* counters) {
+  using WF = WinFin<T, LOGN>;
+  using F = typename WF::F;
+  using CT = C<T>;
+  constexpr int N = WF::N, E = F::E, TPS = WF::TPS, GW = WF::GW, NW = WF::NW;
+  extern __shared__ __align__(16) unsigned char wsm[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g = tid / TPS, tau = tid % TPS;
+  CT* buf = reinterpret_cast<CT*>(wsm) + g * F::NPAD;
+  double* red = reinterpret_cast<double*>(wsm + GW * F::NPAD * (int)sizeof(CT)) + g * NW * 2;
+  // ---- windows: group g of CTA b takes windows (b * GW + g) + k * gridDim.x * GW
+  for (int64_t w = (int64_t)blockIdx.x * GW + g; w < nwin; w += (int64_t)gridDim.x * GW) {
+    const int64_t w0 = w * W, w1 = min(w0 + W, B);
+    CT vi[E], vo[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) vi[k] = vo[k] = mk<T>(0, 0);
+    int64_t c = w0 * G / B;
+    while (c > 0 && c * B / G > w0) --c;
+    while (c < G && (c + 1) * B / G <= w0) ++c;
+    for (; c < G; ++c) {
+      const int64_t lo = c * B / G, hi = (c + 1) * B / G;
+      if (lo >= w1) break;
+      if (hi <= lo) continue;
+      const int64_t j = w - lo / W;
+      for (int q = 0; q < spt; ++q) {
+        const CT* base = ws + ((c * maxseg + j) * spt + q) * 2 * (int64_t)N;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          vi[k] = cadd<T>(vi[k], base[tau + TPS * k]);
+          vo[k] = cadd<T>(vo[k], base[N + tau + TPS * F::out_pos(k)]);
+        }
+      }
+    }
+    F::run(buf, vi, tau, tw, 1 + g);
+    double a2 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const double dr = (double)vi[k].x - (double)vo[k].x, di = (double)vi[k].y - (double)vo[k].y;
+      a2 += dr * dr + di * di;
+      b2 += (double)vi[k].x * (double)vi[k].x + (double)vi[k].y * (double)vi[k].y;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+      b2 += __shfl_xor_sync(0xffffffffu, b2, off);
+    }
+    if constexpr (NW > 1) {
+      if (lane == 0) {
+        red[2 * (tau >> 5)] = a2;
+        red[2 * (tau >> 5) + 1] = b2;
+      }
+      fft_sync_grp<-1, TPS>(1 + g);
+      if (tau == 0) {
+        for (int i = 1; i < NW; ++i) {
+          a2 += red[2 * i];
+          b2 += red[2 * i + 1];
+        }
+      }
+      fft_sync_grp<-1, TPS>(1 + g);  // red[] free for the next window
+    }
+    if (tau == 0) ab.win_div[w] = sqrt(a2) / fmax(sqrt(b2), 1e-30);
+  }
+  // ---- per-signal decisions, a thread per signal: its warps' partials in order
+  double dmax = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + tid; r < B; r += (int64_t)gridDim.x * blockDim.x) {
+    double acc[5] = {0, 0, 0, 0, 0};
+    const double* pp = sig_part + r * nws * 5;
+    for (int i = 0; i < nws; ++i)
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc[q] += pp[i * 5 + q];
+    const double floor_v = sqrt(acc[2]) / sqrt((double)N);
+    double dv;
+    if (!isfinite(acc[3]) || !isfinite(acc[4])) dv = __longlong_as_double(0x7ff0000000000000ll);
+    else dv = hypot(acc[0] - acc[3], acc[1] - acc[4]) / fmax(fmax(hypot(acc[0], acc[1]), floor_v), 1e-30);
+    ab.c_in[2 * r] = acc[0];
+    ab.c_in[2 * r + 1] = acc[1];
+    ab.c_out[2 * r] = acc[3];
+    ab.c_out[2 * r + 1] = acc[4];
+    ab.floors[r] = floor_v;
+    ab.div[r] = dv;
+    if (dv > delta) atomicAdd(&counters->triggered, 1ull);
+    dmax = fmax(dmax, dv);
+  }
+  // one atomic per warp
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+  if (lane == 0 && dmax > 0.0) atomicMax(&counters->max_div_bits, (unsigned long long)__double_as_longlong(dmax));
+}
+
+template <typename T, int LOGN>
+static int launch_wf_t(const void* ws, const double* sig_part, int nws, const void* tw, int64_t B, int64_t W,
+                       int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta, const AbftArgs& ab,
+                       Counters* counters, int num_sms, cudaStream_t st) {
+  using WF = WinFin<T, LOGN>;
+  auto kern = k5_window_finish<T, LOGN>;
+  static LaunchCfg cfg;
+  const int dev = current_device();
+  if (!cfg.done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, WF::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    cfg.done[dev] = true;
+  }
+  if (nwin < 1) return 0;
+  // enough CTAs for the windows (GW per CTA) and for a thread per signal
+  const int64_t want = std::max<int64_t>((nwin + WF::GW - 1) / WF::GW, (B + WF::NT - 1) / WF::NT);
+  const int64_t grid = std::min<int64_t>(want, (int64_t)num_sms * 8);
+  kern<<<(unsigned)grid, WF::NT, WF::SMEM, st>>>(static_cast<const C<T>*>(ws), sig_part, nws,
+                                                  static_cast<const C<T>*>(tw), B, W, G, maxseg, spt, nwin, delta,
+                                                  ab, counters);
+  return (int)cudaGetLastError();
+}
+
+int launch_k5_window_finish(int prec, int logn, const void* ws, const double* sig_part, int nws, const void* tw,
+                            int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta,
+                            const AbftArgs& ab, Counters* counters, int num_sms, cudaStream_t st) {
+#define TFFT_WF(L)                                                                                              \
+  case L:                                                                                                       \
+    return prec == 0 ? launch_wf_t<float, L>(ws, sig_part, nws, tw, B, W, G, maxseg, spt, nwin, delta, ab,     \
+                                             counters, num_sms, st)                                             \
+                     : launch_wf_t<double, L>(ws, sig_part, nws, tw, B, W, G, maxseg, spt, nwin, delta, ab,    \
+                                              counters, num_sms, st);
+  switch (logn) {
+    TFFT_WF(9) TFFT_WF(10) TFFT_WF(11) TFFT_WF(12)
+    case 13:
+      if (prec == 0)
+        return launch_wf_t<float, 13>(ws, sig_part, nws, tw, B, W, G, maxseg, spt, nwin, delta, ab, counters,
+                                      num_sms, st);
+      return (int)cudaErrorInvalidValue;
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+#undef TFFT_WF
+}
+
 template <typename T>
 static int dispatch_k5_abft(int logn, const K1Args* a, int num_sms, cudaStream_t st, int64_t batch, int64_t* grid,
-                            int* spt) {
+                            int* spt, int* nws) {
   switch (logn) {
 #define TFFT_K5A(L)                                                              \
   case L:                                                                        \
     if (spt) *spt = K5<T, L, false, true>::SPT;                                  \
+    if (nws) *nws = K5<T, L, false, true>::NWARP_SLOT;                           \
     if (grid) return k5_grid_t<T, L, false, true>(num_sms, batch, grid);         \
     return launch_k5_t<T, L, false, true>(*a, num_sms, st);
     TFFT_K5A(9) TFFT_K5A(10) TFFT_K5A(11) TFFT_K5A(12)
@@ -534,6 +765,7 @@ static int dispatch_k5_abft(int logn, const K1Args* a, int num_sms, cudaStream_t
     case 13:
       if constexpr (sizeof(T) == 4) {
         if (spt) *spt = K5<T, 13, false, true>::SPT;
+        if (nws) *nws = K5<T, 13, false, true>::NWARP_SLOT;
         if (grid) return k5_grid_t<T, 13, false, true>(num_sms, batch, grid);
         return launch_k5_t<T, 13, false, true>(*a, num_sms, st);
       }
@@ -545,14 +777,14 @@ static int dispatch_k5_abft(int logn, const K1Args* a, int num_sms, cudaStream_t
 
 int launch_k5_abft(int prec, int logn, const K1Args& a, int num_sms, cudaStream_t st) {
   if (!k5_abft_supported(prec, logn)) return (int)cudaErrorInvalidValue;
-  return prec == 0 ? dispatch_k5_abft<float>(logn, &a, num_sms, st, 0, nullptr, nullptr)
-                   : dispatch_k5_abft<double>(logn, &a, num_sms, st, 0, nullptr, nullptr);
+  return prec == 0 ? dispatch_k5_abft<float>(logn, &a, num_sms, st, 0, nullptr, nullptr, nullptr)
+                   : dispatch_k5_abft<double>(logn, &a, num_sms, st, 0, nullptr, nullptr, nullptr);
 }
 
-int k5_abft_layout(int prec, int logn, int num_sms, int64_t batch, int64_t* grid, int* spt) {
+int k5_abft_layout(int prec, int logn, int num_sms, int64_t batch, int64_t* grid, int* spt, int* nws) {
   if (!k5_abft_supported(prec, logn)) return (int)cudaErrorInvalidValue;
-  return prec == 0 ? dispatch_k5_abft<float>(logn, nullptr, num_sms, 0, batch, grid, spt)
-                   : dispatch_k5_abft<double>(logn, nullptr, num_sms, 0, batch, grid, spt);
+  return prec == 0 ? dispatch_k5_abft<float>(logn, nullptr, num_sms, 0, batch, grid, spt, nws)
+                   : dispatch_k5_abft<double>(logn, nullptr, num_sms, 0, batch, grid, spt, nws);
 }
 
 }  // namespace tfft
