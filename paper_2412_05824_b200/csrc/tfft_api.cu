@@ -140,6 +140,7 @@ struct tfft_plan {
   DevBuf scratch_a, scratch_b, base;  // strike path
   DevBuf col_a, col_b, col64;         // single-column work
   K3Plan* k3 = nullptr;               // two-pass machinery (N beyond K1)
+  StagePlan* stg = nullptr;           // three-stage plans: one pass per reference stage
   tfft_plan* promoted = nullptr;      // FP64 twin for FP32 correction columns
 };
 
@@ -273,7 +274,9 @@ int split_faults(tfft_plan* p, const tfft_fault* faults, int nfaults, int64_t si
     if (f.element < 0 || f.element >= p->n || f.stage < 0 || f.stage >= (int)p->spans.size() || f.bit < 0 ||
         f.bit >= (p->prec == 0 ? 32 : 64) || (f.part != 0 && f.part != 1))
       return fail(TFFT_EINVAL, "fault spec out of range");
-    const bool in_kernel = p->mode != 2 && (f.stage == 0 || (k3_split_ok && f.stage == 1 && p->mode == 1 && k3_strikes_stage1(p->k3)));
+    const bool in_kernel = (p->mode == 2 && p->stg) ||
+                           (p->mode != 2 && (f.stage == 0 || (k3_split_ok && f.stage == 1 && p->mode == 1 &&
+                                                              k3_strikes_stage1(p->k3))));
     if (in_kernel) dev.push_back({r, f.element, f.stage, f.part, f.bit, 0});
     else slow.push_back(f);
   }
@@ -361,6 +364,14 @@ int run_plain(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, 
     g_launches.fetch_add(k3_launches(p->k3), std::memory_order_relaxed);
     return rc ? cuda_fail(rc, "k3 launch") : 0;
   }
+  if (p->stg) {
+    int e = p->scratch_b.ensure((size_t)batch * p->n * cbytes(p->prec));
+    if (e) return cuda_fail(e, "stage scratch");
+    int rc = stage_execute(p->stg, x, y, p->scratch_b.p, batch, inverse, (const DevFault*)p->faults.p,
+                           (int)dev.size(), (Counters*)counters, st);
+    g_launches.fetch_add(stage_count(p->stg), std::memory_order_relaxed);
+    return rc ? cuda_fail(rc, "stage pass launch") : 0;
+  }
   return multipass(p, x, y, batch, inverse, counters, st);
 }
 
@@ -443,10 +454,22 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
     if (rc == (int)cudaErrorInvalidValue) {
       p->mode = 2;
       p->k3 = nullptr;
+      // three-stage plans: one stage pass per reference stage when every span
+      // is in the pass kernel's range, else the reference-order radix-4/2 passes
+      if (std::getenv("TFFT_NO_STAGES") == nullptr) {
+        int rs = stage_create(n, precision, p->spans.data(), (int)p->spans.size(), p->num_sms, &p->stg);
+        if (rs && rs != (int)cudaErrorInvalidValue) {
+          tfft_plan_destroy(p);
+          return cuda_fail(rs, "stage plan");
+        }
+        if (rs) p->stg = nullptr;
+      }
     } else if (rc) {
       tfft_plan_destroy(p);
       return cuda_fail(rc, "k3 plan");
     } else {
+      // (two-stage plans keep the fused two-pass kernels: stage passes measured
+      // 1.5-2x slower at 2^17..2^22, the span-2048 passes load 32-byte runs)
       p->mode = 1;
     }
   }
@@ -460,6 +483,7 @@ int tfft_plan_destroy(tfft_plan* p) {
                    &p->ws, &p->win_count, &p->scratch_a, &p->scratch_b, &p->base, &p->col_a, &p->col_b, &p->col64};
   for (DevBuf* b : all) b->release();
   if (p->k3) k3_destroy(p->k3);
+  if (p->stg) stage_destroy(p->stg);
   if (p->promoted) tfft_plan_destroy(p->promoted);
   delete p;
   return TFFT_OK;

@@ -67,6 +67,10 @@ struct ColArgs {
   int nfaults;
   int strike_stage; // stage index whose boundary pass A's output is (1), or -1
   Counters* counters;
+  // MODE 2 (one reference stage as one radix-L Stockham pass):
+  int64_t s;        // S = product of the earlier stages' spans (1 for stage 0)
+  int stage;        // stage index: strikes with this stage flip the loaded legs
+  int last;         // last stage (inverse: x 1/N)
 };
 
 template <typename T, int LOGL, bool INV, int MODE>
@@ -108,13 +112,16 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t sig = t / ncb;
     const int64_t c0 = (t - sig * ncb) * CB;
-    if constexpr (MODE == 0) {
+    if constexpr (MODE == 0 || MODE == 2) {
+      if (MODE == 0 || a.stage == 0) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) bad |= !finite2<T>(ld[i]);
+        for (int i = 0; i < E; ++i) bad |= !finite2<T>(ld[i]);
+      }
       if (a.nfaults > 0) {
+        const int st = MODE == 0 ? 0 : a.stage;
         for (int f = 0; f < a.nfaults; ++f) {
           const DevFault fl = a.faults[f];
-          if (fl.signal != sig || fl.stage != 0) continue;
+          if (fl.signal != sig || fl.stage != st) continue;
 #pragma unroll
           for (int i = 0; i < E; ++i) {
             const int e = i * NT + tid;
@@ -137,8 +144,51 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
     CT v[E];
 #pragma unroll
     for (int k = 0; k < E; ++k) v[k] = slot[F::phys(tau + TPS * k)];
+    if constexpr (MODE == 2) {
+      // DIT Stockham stage: leg t of column j = q + S p' times w_{S L}^{q t}
+      // (= w_N^{q t N / (S L)}, two-level table), then the L-point DFT
+      if (a.s > 1) {
+        const CT* __restrict__ hi = static_cast<const CT*>(a.hi);
+        const CT* __restrict__ lo = static_cast<const CT*>(a.lo);
+        const int64_t lomask = (int64_t(1) << a.lo_bits) - 1;
+        const int64_t q = (c0 + g) & (a.s - 1);
+        const int64_t scale = a.n / (a.s * L);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const int64_t m = q * (int64_t)(tau + TPS * k) * scale;
+          v[k] = cmul<T>(v[k], cmul<T>(__ldg(hi + (m >> a.lo_bits)), __ldg(lo + (m & lomask))));
+        }
+      }
+    }
     F::run(slot, v, tau, tw);
-    if constexpr (MODE == 0) {
+    if constexpr (MODE == 2) {
+      const bool scl = INV && a.last;
+      const T sc = (T)(1.0 / (double)a.n);
+      if (a.s == 1) {
+        // stage 0: column j's L outputs are contiguous at j L + c
+        CT* d = dst + sig * a.n + (c0 + g) * L;
+#pragma unroll
+        for (int k = 0; k < E; ++k) __stcs(d + tau + TPS * F::out_pos(k), scl ? cscale<T>(v[k], sc) : v[k]);
+        __syncthreads();  // tile reuse by the next load
+      } else {
+        // S >= CB: the tile is one p', q = q0 .. q0 + CB - 1; output c of
+        // column q at q + S (L p' + c): L rows of CB contiguous, pitch S
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < E; ++k) slot[F::phys(tau + TPS * F::out_pos(k))] = v[k];
+        __syncthreads();
+        const int64_t q0 = c0 & (a.s - 1), p0 = c0 / a.s;
+        CT* d = dst + sig * a.n + q0 + a.s * L * p0;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int e = i * NT + tid;
+          const int r = e / CB, c = e % CB;
+          const CT val = tile[K::base(c) + F::phys(r)];
+          __stcs(d + (int64_t)r * a.s + c, scl ? cscale<T>(val, sc) : val);
+        }
+        __syncthreads();
+      }
+    } else if constexpr (MODE == 0) {
       // twiddle w_N^{p q} (two-level table) and store Z[p][q] at q + N1 p
       const int64_t p = c0 + g;
       const CT* __restrict__ hi = static_cast<const CT*>(a.hi);
@@ -180,7 +230,7 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
       __syncthreads();
     }
   }
-  if constexpr (MODE == 0) {
+  if constexpr (MODE == 0 || MODE == 2) {
     if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
   }
 }
@@ -221,6 +271,11 @@ static int dispatch_col(int logl, const ColArgs& a, int num_sms, cudaStream_t st
 }
 
 static int col(int prec, bool inv, int mode, int logl, const ColArgs& a, int num_sms, cudaStream_t st) {
+  if (mode == 2) {
+    if (prec == 0)
+      return inv ? dispatch_col<float, true, 2>(logl, a, num_sms, st) : dispatch_col<float, false, 2>(logl, a, num_sms, st);
+    return inv ? dispatch_col<double, true, 2>(logl, a, num_sms, st) : dispatch_col<double, false, 2>(logl, a, num_sms, st);
+  }
   if (prec == 0) {
     if (mode == 0) return inv ? dispatch_col<float, true, 0>(logl, a, num_sms, st) : dispatch_col<float, false, 0>(logl, a, num_sms, st);
     return inv ? dispatch_col<float, true, 1>(logl, a, num_sms, st) : dispatch_col<float, false, 1>(logl, a, num_sms, st);
@@ -291,6 +346,99 @@ int ilog2i(int64_t v) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// stage passes
+
+struct StagePlan {
+  int64_t n = 0;
+  int prec = 0;
+  int nst = 0;
+  int64_t spans[3] = {0, 0, 0};
+  int lo_bits = 0;
+  int num_sms = 148;
+  void* tw[3][2] = {};  // omega_span^m per stage (conj for inverse)
+  void* hi[2] = {nullptr, nullptr};
+  void* lo[2] = {nullptr, nullptr};
+};
+
+int stage_create(int64_t n, int prec, const int64_t* spans, int nstages, int num_sms, StagePlan** out) {
+  *out = nullptr;
+  if (nstages < 2 || nstages > 3) return (int)cudaErrorInvalidValue;
+  for (int k = 0; k < nstages; ++k)
+    if (spans[k] < 64 || spans[k] > 2048) return (int)cudaErrorInvalidValue;  // col_kernel's L range
+  StagePlan* p = new StagePlan();
+  p->n = n;
+  p->prec = prec;
+  p->nst = nstages;
+  p->num_sms = num_sms;
+  const int logn = ilog2i(n);
+  p->lo_bits = (logn + 1) / 2;
+  int e = 0;
+  for (int k = 0; k < nstages && !e; ++k) {
+    p->spans[k] = spans[k];
+    for (int c = 0; c < 2 && !e; ++c) e = upload_table(prec, spans[k], 1, spans[k], c == 1, &p->tw[k][c]);
+  }
+  for (int c = 0; c < 2 && !e; ++c) {
+    e = upload_table(prec, n, int64_t(1) << p->lo_bits, n >> p->lo_bits, c == 1, &p->hi[c]);
+    if (!e) e = upload_table(prec, n, 1, int64_t(1) << p->lo_bits, c == 1, &p->lo[c]);
+  }
+  if (e) {
+    stage_destroy(p);
+    return e;
+  }
+  *out = p;
+  return 0;
+}
+
+void stage_destroy(StagePlan* p) {
+  if (!p) return;
+  for (auto& t : p->tw)
+    for (void* q : t) cudaFree(q);
+  for (int c = 0; c < 2; ++c) {
+    cudaFree(p->hi[c]);
+    cudaFree(p->lo[c]);
+  }
+  delete p;
+}
+
+int stage_count(const StagePlan* p) { return p ? p->nst : 0; }
+
+int stage_execute(StagePlan* p, const void* x, void* y, void* tmp, int64_t batch, int inverse, const DevFault* faults,
+                  int nfaults, Counters* counters, cudaStream_t st) {
+  const int c = inverse ? 1 : 0;
+  const void* src = x;
+  int64_t S = 1;
+  for (int k = 0; k < p->nst; ++k) {
+    // ping-pong ending in y: ..., tmp, y
+    void* dst = ((p->nst - 1 - k) % 2 == 0) ? y : tmp;
+    const int64_t L = p->spans[k];
+    ColArgs a{};
+    a.src = src;
+    a.dst = dst;
+    a.batch = batch;
+    a.n = p->n;
+    a.pitch = p->n / L;
+    a.ncols = p->n / L;
+    a.n1 = 0;
+    a.tw = p->tw[k][c];
+    a.hi = p->hi[c];
+    a.lo = p->lo[c];
+    a.lo_bits = p->lo_bits;
+    a.faults = faults;
+    a.nfaults = nfaults;
+    a.strike_stage = -1;
+    a.counters = counters;
+    a.s = S;
+    a.stage = k;
+    a.last = k == p->nst - 1;
+    const int rc = col(p->prec, inverse != 0, 2, ilog2i(L), a, p->num_sms, st);
+    if (rc) return rc;
+    src = dst;
+    S *= L;
+  }
+  return 0;
+}
 
 int k3_create(int64_t n, int prec, const int64_t* spans, int nstages, int num_sms, K3Plan** out) {
   *out = nullptr;

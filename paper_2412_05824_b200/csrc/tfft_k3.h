@@ -28,4 +28,16 @@ int k3_launches(const K3Plan* p);
 const void* k3_enc_table(K3Plan* p);
 const void* k3_enc_table_inv(K3Plan* p);
 
+// Stage passes (three-stage plans, N = 2^23..2^25): one launch per reference
+// stage, each a radix-span Stockham pass over the batch, so every stage
+// boundary is a kernel boundary (strikes of any stage land in-kernel) and
+// the transform costs nstages HBM round trips instead of one per radix-4 pass.
+struct StagePlan;
+int stage_create(int64_t n, int prec, const int64_t* spans, int nstages, int num_sms, StagePlan** out);
+void stage_destroy(StagePlan* p);
+// x -> y through tmp (batch * n elements); faults of any stage (signal rows local)
+int stage_execute(StagePlan* p, const void* x, void* y, void* tmp, int64_t batch, int inverse, const DevFault* faults,
+                  int nfaults, Counters* counters, cudaStream_t st);
+int stage_count(const StagePlan* p);
+
 }  // namespace tfft
