@@ -19,6 +19,24 @@
 
 namespace tfft {
 
+// Single-column work of the replay runs at full width: CTA c owns the
+// 8192-element chunk c and writes its partials; a one-warp finisher combines
+// the chunks in order (deterministic). The partials live in a per-device
+// scratch (the replay is serial per device; 2^29 / 8192 chunks x 2 doubles).
+constexpr int64_t kChunk = 8192;
+
+double* chunk_scratch() {
+  static double* buf[kMaxDevices] = {};
+  const int d = current_device();
+  if (!buf[d]) {
+    if (cudaMalloc(&buf[d], (size_t)((int64_t(1) << 29) / kChunk) * 2 * sizeof(double)) != cudaSuccess) {
+      buf[d] = nullptr;
+    }
+  }
+  return buf[d];
+}
+
+
 // ---------------------------------------------------------------------------
 
 template <typename T, bool INV>
@@ -546,6 +564,11 @@ __global__ void __launch_bounds__(256) group_div_kernel(const C<T>* ref, const C
 }
 
 int launch_group_div(int prec, const void* ref, const void* s_out, int64_t n, double* out, cudaStream_t st) {
+  if (n >= 65536) {  // one long row: chunk partials at full width, combined in order
+    double* part = chunk_scratch();
+    if (!part) return (int)cudaErrorMemoryAllocation;
+    return launch_group_div_chunked(prec, ref, s_out, n, 1, out, part, st);
+  }
   return launch_group_div_batched(prec, ref, s_out, n, 1, out, st);
 }
 
@@ -624,10 +647,11 @@ int launch_group_div_batched(int prec, const void* ref, const void* s_out, int64
 
 template <typename T>
 __global__ void __launch_bounds__(256) correction_column_kernel(const C<T>* snap_out, const double2* ref64, int64_t n,
-                                                                double weight, C<T>* col, double* res) {
+                                                                double weight, C<T>* col, double* part) {
   __shared__ double sh[8 * 2];
   double acc[2] = {0, 0};  // [0] non-finite count, [1] max |col|
-  for (int64_t k = threadIdx.x; k < n; k += 256) {
+  const int64_t k0 = blockIdx.x * kChunk, k1 = min(k0 + kChunk, n);
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += 256) {
     const double re = ((double)snap_out[k].x - ref64[k].x) / weight;
     const double im = ((double)snap_out[k].y - ref64[k].y) / weight;
     const C<T> c = mk<T>((T)re, (T)im);
@@ -653,8 +677,30 @@ __global__ void __launch_bounds__(256) correction_column_kernel(const C<T>* snap
       bad += sh[2 * i];
       mx = fmax(mx, sh[2 * i + 1]);
     }
-    res[0] = bad == 0 ? 1.0 : 0.0;
-    res[1] = mx;
+    part[2 * blockIdx.x] = bad;
+    part[2 * blockIdx.x + 1] = mx;
+  }
+}
+
+// mode 0: res[0] = all finite, res[1] = max; mode 1: res[2..3] = sums
+__global__ void chunk_finish_kernel(const double* part, int64_t nchunk, int mode, double* res) {
+  if (threadIdx.x != 0) return;
+  double a = 0, b = 0;
+  for (int64_t c = 0; c < nchunk; ++c) {
+    if (mode == 0) {
+      a += part[2 * c];
+      b = fmax(b, part[2 * c + 1]);
+    } else {
+      a += part[2 * c];
+      b += part[2 * c + 1];
+    }
+  }
+  if (mode == 0) {
+    res[0] = a == 0 ? 1.0 : 0.0;
+    res[1] = b;
+  } else {
+    res[2] = a;
+    res[3] = b;
   }
 }
 
@@ -662,21 +708,26 @@ __global__ void __launch_bounds__(256) correction_column_kernel(const C<T>* snap
 // the column is (snap_out - ref) / w with ref in the same precision.
 int launch_correction_column(int prec, const void* snap_out, const void* ref64, int64_t n, double weight, void* col,
                              double* res, cudaStream_t st) {
+  double* part = chunk_scratch();
+  if (!part) return (int)cudaErrorMemoryAllocation;
+  const int64_t nc = (n + kChunk - 1) / kChunk;
   if (prec == 0)
-    correction_column_kernel<float><<<1, 256, 0, st>>>((const float2*)snap_out, (const double2*)ref64, n, weight,
-                                                      (float2*)col, res);
+    correction_column_kernel<float><<<(unsigned)nc, 256, 0, st>>>((const float2*)snap_out, (const double2*)ref64, n,
+                                                                  weight, (float2*)col, part);
   else
-    correction_column_kernel<double><<<1, 256, 0, st>>>((const double2*)snap_out, (const double2*)ref64, n, weight,
-                                                       (double2*)col, res);
+    correction_column_kernel<double><<<(unsigned)nc, 256, 0, st>>>((const double2*)snap_out, (const double2*)ref64, n,
+                                                                   weight, (double2*)col, part);
+  chunk_finish_kernel<<<1, 32, 0, st>>>(part, nc, 0, res);
   return (int)cudaGetLastError();
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) patch_row_kernel(C<T>* yk, const C<T>* col, int64_t n, int enc,
-                                                        const C<T>* tw, double* res) {
+                                                        const C<T>* tw, double* part) {
   __shared__ double sh[8 * 2];
   C<T> co = mk<T>(0, 0);
-  for (int64_t k = threadIdx.x; k < n; k += 256) {
+  const int64_t k0 = blockIdx.x * kChunk, k1 = min(k0 + kChunk, n);
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += 256) {
     const C<T> v = csub<T>(yk[k], col[k]);
     yk[k] = v;
     co = cadd<T>(co, cmul<T>(enc_value<T>(enc, k, n, tw), v));
@@ -684,21 +735,26 @@ __global__ void __launch_bounds__(256) patch_row_kernel(C<T>* yk, const C<T>* co
   double acc[2] = {(double)co.x, (double)co.y};
   block_sum256<2>(acc, sh);
   if (threadIdx.x == 0) {
-    res[2] = acc[0];
-    res[3] = acc[1];
+    part[2 * blockIdx.x] = acc[0];
+    part[2 * blockIdx.x + 1] = acc[1];
   }
 }
 
 int launch_patch_row(int prec, void* yk, const void* col, int64_t n, int enc, const void* tw, double* res,
                      cudaStream_t st) {
+  double* part = chunk_scratch();
+  if (!part) return (int)cudaErrorMemoryAllocation;
+  const int64_t nc = (n + kChunk - 1) / kChunk;
   if (prec == 0)
-    patch_row_kernel<float><<<1, 256, 0, st>>>((float2*)yk, (const float2*)col, n, enc, (const float2*)tw, res);
+    patch_row_kernel<float><<<(unsigned)nc, 256, 0, st>>>((float2*)yk, (const float2*)col, n, enc, (const float2*)tw,
+                                                         part);
   else
-    patch_row_kernel<double><<<1, 256, 0, st>>>((double2*)yk, (const double2*)col, n, enc, (const double2*)tw, res);
+    patch_row_kernel<double><<<(unsigned)nc, 256, 0, st>>>((double2*)yk, (const double2*)col, n, enc,
+                                                          (const double2*)tw, part);
+  chunk_finish_kernel<<<1, 32, 0, st>>>(part, nc, 1, res);
   return (int)cudaGetLastError();
 }
 
-// promote / demote a column between working precision and FP64
 __global__ void promote_kernel(const float2* in, double2* out, int64_t n) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
     out[k] = make_double2(in[k].x, in[k].y);

@@ -14,8 +14,8 @@ import paper_2412_05824_b200 as tf
 from paper_2412_05824_b200 import fft_core
 
 
-def run(prec, bpc, profile=False):
-    n = 2 ** 22
+def run(prec, bpc, profile=False, logn=22, bit=None):
+    n = 2 ** logn
     b = 2 ** 31 // (n * bpc)
     rdt = torch.float32 if prec == "single" else torch.float64
     cdt = torch.complex64 if prec == "single" else torch.complex128
@@ -30,7 +30,7 @@ def run(prec, bpc, profile=False):
     for w in range(nwin):
         tx = w * T + int(rng.integers(0, T))
         inj.arm(tf.FaultSpec(transaction=tx, signal=tx * plan.bs, element=int(rng.integers(0, n)), stage=0, part="re",
-                             bit=30 if prec == "single" else 62), plan=plan, batch=batch)
+                             bit=bit if bit is not None else (30 if prec == "single" else 62)), plan=plan, batch=batch)
     fft_core.device_execute(plan, xd, yd)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -60,5 +60,8 @@ def run(prec, bpc, profile=False):
 
 if __name__ == "__main__":
     prof = "--profile" in sys.argv
-    run("single", 8, prof)
-    run("double", 16, prof)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    logn = int(args[0]) if args else 22
+    bits = (int(args[1]), int(args[2])) if len(args) > 2 else (None, None)
+    run("single", 8, prof, logn, bits[0])
+    run("double", 16, prof, logn, bits[1])
