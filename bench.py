@@ -280,8 +280,7 @@ def run_ours(args, dist):
         gbs = 2 * n * b * 16 / t / 1e9
         sweep.append({"n": n, "batch": b, "ms": round(t * 1e3, 4), "gflops": round(FLOP(n) * b / t / 1e9, 1),
                       "gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
-                      "kernel": "k1_single_pass" if n <= 256 else ("k5_single_pass" if n <= 4096 else
-                                                                                   "k7_fused_two_pass")})
+                      "kernel": _kernel_label("double", n)})
     dom = max(range(len(sizes)), key=lambda i: statistics.mean(per_n[i]))
     dn = sweep[dom]
     roofline = {"bound": "hbm", "achieved": dn["gbs"], "peak": peak, "unit": "GB/s",
@@ -309,8 +308,11 @@ def run_ours(args, dist):
     }
     del x, y
     torch.cuda.empty_cache()
+    out["sweep_fp32"] = fp32_sweep(args, dist, peak)
     if not args.no_abft:
         out["abft"] = abft_overheads(args, dist)
+        out["abft_T_sweep"] = abft_t_sweep(args, dist)
+        out["c4"] = c4_config(args, dist, peak)
     out["c1"] = c1_config(args, dist)
     if not args.no_e2e:
         out["e2e"] = e2e(args, dist, sizes, plans, total_elems)
@@ -385,13 +387,150 @@ def abft_overheads(args, dist):
         res[name] = {"n": n, "batch_per_gpu": b, "T": T, "bs": plan.bs, "plain_ms": round(tp * 1e3, 4),
                      "fused_ms": round(tfz * 1e3, 4), "overhead_pct": round(100 * (tfz / tp - 1), 2),
                      "plain_gbs": round(gbs, 1),
-                     "path": "K5 transform + one-sweep checksums (measured faster than the fused K5 from 2^11)"
+                     "path": "K5 with fused two-sided ABFT (window sums in TMEM) + one window-finisher launch"
                              if n <= 4096 else ("K7" if prec == "double" else "K4") + " transform + one-sweep checksums"}
         if api is not None:
             res[name]["public_api"] = api
         del x, y, sums
         torch.cuda.empty_cache()
     return res
+
+
+def _kernel_label(prec, n):
+    logn = int(np.log2(n))
+    if logn <= 8:
+        return "k1_single_pass"
+    if logn <= (13 if prec == "single" else 12):
+        return "k5_single_pass"
+    if logn <= 22:
+        return ("k7" if prec == "double" and logn <= 20 else "k4/k3") + "_two_pass"
+    return "stage_passes"
+
+
+def fp32_sweep(args, dist, peak):
+    """FP32 N=2^8..2^20 at 1 GiB per N (north_star: FP32 and FP64 2^8..2^20),
+    device-resident, CUDA events, median of the timed steps."""
+    import torch
+
+    import paper_2412_05824_b200 as tf
+    from paper_2412_05824_b200 import fft_core
+
+    total = 2 ** 27  # complex64 elements = 1 GiB
+    x = torch.randn(total * 2, dtype=torch.float32, device="cuda").view(torch.complex64)
+    y = torch.empty_like(x)
+    rows = []
+    for n in sweep_sizes(args.sweep):
+        b = total // n
+        plan = tf.build_plan(tf.select_params(n, b, "single"), "single")
+        xv, yv = x.view(-1, n), y.view(-1, n)
+        t = _time_loop(lambda: fft_core.device_execute(plan, xv, yv), max(args.steps, 5), args.warmup, dist)
+        gbs = 2 * n * b * 8 / t / 1e9
+        rows.append({"n": n, "batch": b, "ms": round(t * 1e3, 4), "gflops": round(FLOP(n) * b / t / 1e9, 1),
+                     "gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4), "kernel": _kernel_label("single", n)})
+    del x, y
+    torch.cuda.empty_cache()
+    return rows
+
+
+def abft_t_sweep(args, dist):
+    """C3 (N=4096, 1 GiB, fault-free) fused-ABFT overhead for T in {1,2,4,8,16,32}."""
+    import torch
+
+    import paper_2412_05824_b200 as tf
+    from paper_2412_05824_b200 import abft as A, fft_core
+
+    res = {}
+    for prec, b in (("single", 32768), ("double", 16384)):
+        dt = torch.complex64 if prec == "single" else torch.complex128
+        rdt = torch.float32 if prec == "single" else torch.float64
+        n = 4096
+        x = torch.randn(b * n * 2, dtype=rdt, device="cuda").view(dt).view(b, n)
+        y = torch.empty_like(x)
+        plan = tf.build_plan(tf.select_params(n, b, prec), prec)
+        tp = _time_loop(lambda: fft_core.device_execute(plan, x, y), max(args.steps, 5), args.warmup, dist)
+        row = {"plain_ms": round(tp * 1e3, 4)}
+        for T in (1, 2, 4, 8, 16, 32):
+            nwin = -(-(-(-b // plan.bs)) // T)
+            sums = A._DeviceSums(b, nwin)
+            delta = A.default_delta(prec)
+            tf_ = _time_loop(lambda: A.protected_device(plan, x, y, delta=delta, group_size=T,
+                                                        counters=sums.counters, sums=sums),
+                             max(args.steps, 5), args.warmup, dist)
+            row[f"T{T}"] = {"ms": round(tf_ * 1e3, 4), "overhead_pct": round(100 * (tf_ / tp - 1), 2)}
+        res[f"C3_{'fp32' if prec == 'single' else 'fp64'}_n4096"] = row
+        del x, y
+        torch.cuda.empty_cache()
+    return res
+
+
+def c4_config(args, dist, peak):
+    """C4: large N under injection. N=2^22 (two stages, bs=1) and 2^23 (three
+    stages, curated (256,128,256) bs=16), FP32 and FP64, 2 GiB in. Clean: plain
+    vs protected (device). Injected: run_protected through the public API on
+    the device batch with one exponent/mantissa fault per verification window
+    (T=2 at 2^22: 32 FP32 / 16 FP64 injections), wall clock of the whole call
+    (transform, checksums, host replay, corrections or recomputations)."""
+    import torch
+
+    import paper_2412_05824_b200 as tf
+    from paper_2412_05824_b200 import abft as A, fft_core
+
+    out = {}
+    for logn in (22, 23):
+        n = 2 ** logn
+        for prec, bpc in (("single", 8), ("double", 16)):
+            b = 2 ** 31 // (n * bpc)
+            dt = torch.complex64 if prec == "single" else torch.complex128
+            rdt = torch.float32 if prec == "single" else torch.float64
+            x = torch.randn(b * n * 2, dtype=rdt, device="cuda").view(dt).view(b, n)
+            y = torch.empty_like(x)
+            plan = tf.build_plan(tf.select_params(n, b, prec), prec)
+            T = 2 if logn == 22 else 1
+            nwin = -(-(-(-b // plan.bs)) // T)
+            sums = A._DeviceSums(b, nwin)
+            delta = A.default_delta(prec)
+            steps = max(2, min(args.steps, 5))
+            tp = _time_loop(lambda: fft_core.device_execute(plan, x, y), steps, 1, dist)
+            tq = _time_loop(lambda: A.protected_device(plan, x, y, delta=delta, group_size=T,
+                                                       counters=sums.counters, sums=sums), steps, 1, dist)
+            gbs = 2 * n * b * bpc / tp / 1e9
+            row = {"n": n, "batch": b, "bs": plan.bs, "stages": [st.span for st in plan.stages], "T": T, "plain_ms": round(tp * 1e3, 3), "plain_gbs": round(gbs, 1),
+                   "hbm_frac": round(gbs / peak, 4), "protected_clean_ms": round(tq * 1e3, 3),
+                   "clean_overhead_pct": round(100 * (tq / tp - 1), 2), "path": _kernel_label(prec, n)}
+            if logn == 22:
+                batch = tf.SignalBatch(x)
+                rng = np.random.default_rng(0xC4)
+                # mantissa-top bit: the per-signal test fires and the fault is corrected online
+                bit = 22 if prec == "single" else 51
+                specs = []
+                for w in range(nwin):
+                    tx = w * T + int(rng.integers(0, T))
+                    specs.append(tf.FaultSpec(transaction=tx, signal=tx * plan.bs, element=int(rng.integers(0, n)),
+                                              stage=int(rng.integers(0, 2)), part="re", bit=bit))
+                tf.run_protected(plan, batch, group_size=T)  # warm (row, workspaces)
+                torch.cuda.synchronize()
+                inj = tf.FaultInjector(seu=False)
+                for sp in specs:
+                    inj.arm(sp, plan=plan, batch=batch)
+                stats = tf.RunStats()
+                t0 = time.perf_counter()
+                tf.run_protected(plan, batch, group_size=T, injector=inj, stats=stats)
+                torch.cuda.synchronize()
+                ti = dist.max(time.perf_counter() - t0)
+                t0 = time.perf_counter()
+                tf.run_protected(plan, batch, group_size=T)
+                torch.cuda.synchronize()
+                tc = dist.max(time.perf_counter() - t0)
+                row["injected"] = {"injections": len(specs), "bit": bit, "events": len(stats.events),
+                                   "corrections": stats.corrections, "recomputations": stats.recomputations,
+                                   "api_clean_ms": round(tc * 1e3, 2), "api_injected_ms": round(ti * 1e3, 2),
+                                   "injection_overhead_pct": round(100 * (ti / tc - 1), 1),
+                                   "per_event_ms": round((ti - tc) * 1e3 / max(len(stats.events), 1), 3),
+                                   "call": "run_protected(SignalBatch(device tensor), group_size=T, injector)"}
+            out[f"{'fp32' if prec == 'single' else 'fp64'}_2p{logn}"] = row
+            del x, y, sums
+            torch.cuda.empty_cache()
+    return out
 
 
 def c5_public_api(plan, x, b, T, dist, steps, warmup):
