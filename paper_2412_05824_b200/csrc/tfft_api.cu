@@ -606,15 +606,50 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     a.abft = ab;
     TFFT_TRY(launch_k1(p->prec, p->logn, false, true, a, p->num_sms, st), "k1 abft launch");
   } else {
-    // two-pass / multipass sizes: transform (strikes included), then checksum
-    // and window sweeps over x and y on the device (not fused yet)
+    const size_t cb = cbytes(p->prec);
+    // two-pass sizes on K4, opt-in (TFFT_K4_ABFT=1): the checksums fused into
+    // the transform's launch (C tiles over L2-resident x and y), then the
+    // window FFT, the group divergence and the per-signal decisions. Correct
+    // (the GPU suite passes with it on) but measured slower than plain K4 +
+    // one sweep at C5 (2.0-2.4 vs 1.45 ms): the C tiles' re-reads evict the
+    // L2 ring (5.2 GB DRAM at 32-signal groups) or, with one window per group,
+    // the schedule loses its parallelism (2.3 ms at 3.2 GB). DESIGN.md (d).
+    if (p->mode == 1 && slow.empty() && !abft_force_sweep() && std::getenv("TFFT_K4_ABFT") != nullptr) {
+      int e = p->wsum.ensure((size_t)3 * nwin * p->n * cb);
+      const int64_t nchunk_max = p->n / 256;
+      if (!e) e = p->sigpart.ensure((size_t)batch * nchunk_max * 5 * sizeof(double));
+      if (!e) e = p->part.ensure((size_t)nwin * ((p->n + 8191) / 8192) * 2 * sizeof(double));
+      if (!e) e = p->counters.ensure(8 * sizeof(uint64_t));
+      if (e) return cuda_fail(e, "fused abft workspace");
+      char* s_in = (char*)p->wsum.p;
+      char* s_out = s_in + (size_t)nwin * p->n * cb;
+      char* ref = s_out + (size_t)nwin * p->n * cb;
+      int64_t nparts = 0;
+      int rk = k3_protected(p->k3, x, y, batch, signal_offset, (const DevFault*)p->faults.p, (int)dev.size(),
+                            (Counters*)counters, ab, p->rows[enc].p, s_in, s_out, (double*)p->sigpart.p, &nparts,
+                            st);
+      if (rk != (int)cudaErrorNotSupported) {
+        if (rk) return cuda_fail(rk, "fused k4 abft launch");
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        TFFT_TRY(launch_signal_epilogue((const double*)p->sigpart.p, nparts, p->n, batch, delta, ab,
+                                        (Counters*)counters, st),
+                 "abft signal epilogue");
+        std::vector<DevFault> none;
+        rc = run_plain(p, s_in, ref, nwin, 0, 0, none, (uint64_t*)p->counters.p + 4, st);
+        if (rc) return rc;
+        TFFT_TRY(launch_group_div_chunked(p->prec, ref, s_out, p->n, nwin, sums->win_div, (double*)p->part.p, st),
+                 "window group div");
+        return TFFT_OK;
+      }
+    }
+    // other two-pass / multipass sizes: transform (strikes included), then
+    // checksum and window sweeps over x and y on the device
     rc = run_plain(p, x, y, batch, 0, signal_offset, dev, counters, st);
     if (rc) return rc;
     if (!slow.empty()) {
       rc = strike_path(p, x, y, batch, 0, signal_offset, slow, st, nullptr);
       if (rc) return rc;
     }
-    const size_t cb = cbytes(p->prec);
     int e = p->wsum.ensure((size_t)3 * nwin * p->n * cb);
     if (!e) e = p->part.ensure((size_t)batch * window_sweep_chunks(p->n) * 8 * 5 * sizeof(double));
     if (e) return cuda_fail(e, "window sums");

@@ -664,9 +664,96 @@ int k3_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, co
   return col(p->prec, inverse != 0, 1, p->l2, b, p->num_sms, st);
 }
 
-int k3_protected(K3Plan*, const void*, void*, int64_t, int64_t, const DevFault*, int, Counters*, const AbftArgs&,
-                 const void*, cudaStream_t) {
-  return (int)cudaErrorNotSupported;  // protected runs over K3 use the unfused device path (tfft_api.cu)
+// Fused two-sided ABFT on the K4 schedule (forward): the transform plus the C
+// tiles that form the window sums and per-(signal, chunk) checksum partials
+// from x and y while they are L2-resident. cudaErrorNotSupported when the
+// split runs on K7 / K3, the window does not divide into the group size, or
+// the batch needs several launches; the caller then uses the checksum sweep.
+int k3_protected(K3Plan* p, const void* x, void* y, int64_t batch, int64_t weight0, const DevFault* faults,
+                 int nfaults, Counters* counters, const AbftArgs& ab, const void* row, void* s_in, void* s_out,
+                 double* sig_part, int64_t* nparts, cudaStream_t st) {
+  if (!p->k4 || (p->prec == 1 && k7_supported(p->l1, p->l2) && std::getenv("TFFT_NO_K7") == nullptr))
+    return (int)cudaErrorNotSupported;
+  if (ab.enc != ENC_WANG && ab.enc != ENC_ONES) return (int)cudaErrorNotSupported;
+  const int64_t W = ab.win_signals;
+  const int64_t G0 = k4_group(p, batch);
+  if (W > 2 * G0) return (int)cudaErrorNotSupported;  // ring would outgrow L2
+  // a smaller group than the plain schedule's: the C tiles' x / y reads
+  // share the L2 with the ring (TFFT_K4_ABFT_G: windows per group)
+  int64_t gw = 1;
+  if (const char* e = std::getenv("TFFT_K4_ABFT_G")) gw = std::atoll(e) > 0 ? std::atoll(e) : 1;
+  int64_t G = gw * W;
+  if (G > 2 * G0) G = W;
+  const int64_t rows = int64_t(1) << (p->l1 > p->l2 ? p->l1 : p->l2);
+  if (batch > (int64_t(1) << 31) / rows - 1) return (int)cudaErrorNotSupported;
+  const int64_t KC = k4_abft_chunk(p->prec, p->l1, p->l2);
+  if (p->n % KC) return (int)cudaErrorNotSupported;
+  const size_t cb = p->prec == 0 ? 8 : 16;
+  const size_t ring = (size_t)3 * G * p->n * cb;
+  if (p->ring_cap < ring) {
+    cudaFree(p->ring);
+    p->ring = nullptr;
+    p->ring_cap = 0;
+    cudaError_t e = cudaMalloc(&p->ring, ring);
+    if (e != cudaSuccess) return (int)e;
+    p->ring_cap = ring;
+  }
+  const int64_t ng = (batch + G - 1) / G;
+  const int64_t nwin = (batch + W - 1) / W;
+  const size_t sync = 8 + (size_t)(2 * ng + nwin) * sizeof(unsigned);
+  if (p->sync_cap < sync) {
+    cudaFree(p->sync);
+    p->sync = nullptr;
+    p->sync_cap = 0;
+    cudaError_t e = cudaMalloc(&p->sync, sync);
+    if (e != cudaSuccess) return (int)e;
+    p->sync_cap = sync;
+  }
+  cudaError_t e = cudaMemsetAsync(p->sync, 0, sync, st);
+  if (e != cudaSuccess) return (int)e;
+  const int64_t N1 = int64_t(1) << p->l1, N2 = int64_t(1) << p->l2;
+  const int lmax = p->l1 > p->l2 ? p->l1 : p->l2;
+  const int64_t tpa = N2 / k4_columns_per_tile(p->prec, p->l1, lmax);
+  const int64_t tpb = N1 / k4_columns_per_tile(p->prec, p->l2, lmax);
+  const int64_t glast = batch - (ng - 1) * G;
+  const int64_t nchunk = p->n / KC;
+  K4Args a{};
+  a.x = x;
+  a.y = y;
+  a.z = p->ring;
+  a.batch = batch;
+  a.group = G;
+  a.ngroups = ng;
+  a.ta = G * tpa;
+  a.tb = G * tpb;
+  a.ta_last = glast * tpa;
+  a.tb_last = glast * tpb;
+  a.tw1 = p->tw1[0];
+  a.tw2 = p->tw2[0];
+  a.hi = p->hi[0];
+  a.lo = p->lo[0];
+  a.lo_bits = p->lo_bits;
+  a.faults = faults;
+  a.nfaults = nfaults;
+  a.strike_stage = p->stage1 ? 1 : -1;
+  a.counters = counters;
+  a.ticket = static_cast<unsigned long long*>(p->sync);
+  a.done_a = reinterpret_cast<unsigned*>(static_cast<char*>(p->sync) + 8);
+  a.done_b = a.done_a + ng;
+  a.abft = 1;
+  a.enc = ab.enc;
+  a.win = W;
+  a.tc = (G / W) * nchunk;
+  a.tc_last = ((glast + W - 1) / W) * nchunk;
+  a.nchunk = nchunk;
+  a.weight0 = weight0;
+  a.row = row;
+  a.s_in = s_in;
+  a.s_out = s_out;
+  a.sig_part = sig_part;
+  a.done_w = a.done_b + ng;
+  *nparts = nchunk;
+  return launch_k4_abft(p->prec, p->l1, p->l2, a, p->num_sms, st);
 }
 
 int k3_base_table(K3Plan*, int prec, int64_t s, int r, int inverse, void* dst, cudaStream_t st) {

@@ -15,8 +15,12 @@ int k3_create(int64_t n, int prec, const int64_t* spans, int nstages, int num_sm
 void k3_destroy(K3Plan* p);
 int k3_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, const DevFault* faults, int nfaults,
                Counters* counters, void* reserved, cudaStream_t st);
+// fused two-sided ABFT on the K4 schedule (forward); cudaErrorNotSupported
+// when not applicable. Outputs s_in / s_out [nwin][n] and [B][*nparts][5]
+// per-signal checksum partials (launch_signal_epilogue decides them).
 int k3_protected(K3Plan* p, const void* x, void* y, int64_t batch, int64_t weight0, const DevFault* faults,
-                 int nfaults, Counters* counters, const AbftArgs& ab, const void* row, cudaStream_t st);
+                 int nfaults, Counters* counters, const AbftArgs& ab, const void* row, void* s_in, void* s_out,
+                 double* sig_part, int64_t* nparts, cudaStream_t st);
 // omega_(s r)^q for q < s into dst (working precision, conj for inverse)
 int k3_base_table(K3Plan* p, int prec, int64_t s, int r, int inverse, void* dst, cudaStream_t st);
 // true when the two-pass split equals the reference's first stage span, so

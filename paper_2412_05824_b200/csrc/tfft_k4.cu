@@ -114,8 +114,8 @@ struct K4Item {
   int64_t r;
 };
 
-__device__ __forceinline__ K4Item k4_decode(const K4Args& a, int64_t t) {
-  const int64_t ta = a.ta, tb = a.tb, ng = a.ngroups, taL = a.ta_last, tbL = a.tb_last;
+__device__ __forceinline__ K4Item k4_decode_ab(const K4Args& a, int64_t t) {
+  const int64_t ta = a.ta, tb = a.tb + a.tc, ng = a.ngroups, taL = a.ta_last, tbL = a.tb_last + a.tc_last;
   if (ng == 1) {
     if (t < taL) return {0, 0, t};
     t -= taL;
@@ -139,14 +139,40 @@ __device__ __forceinline__ K4Item k4_decode(const K4Args& a, int64_t t) {
   return {-1, 0, 0};
 }
 
+// phase 2 = a C tile (fused ABFT): index r past the group's B tiles
+__device__ __forceinline__ K4Item k4_decode(const K4Args& a, int64_t t) {
+  K4Item it = k4_decode_ab(a, t);
+  if (it.phase == 1) {
+    const int64_t tbg = it.g == a.ngroups - 1 ? a.tb_last : a.tb;
+    if (it.r >= tbg) {
+      it.phase = 2;
+      it.r -= tbg;
+    }
+  }
+  return it;
+}
+
 __device__ __forceinline__ bool k4_ready(const K4Args& a, const K4Item& it) {
   if (it.phase == 0) {
     if (it.g < 3) return true;
     return ld_acquire(a.done_b + (it.g - 3)) >= (unsigned)a.tb;
   }
+  if (it.phase == 2) {
+    // every B tile of the window's signals has stored its outputs
+    const int64_t w = it.g * (a.group / a.win) + it.r / a.nchunk;
+    const int64_t w0 = w * a.win, w1 = w0 + a.win < a.batch ? w0 + a.win : a.batch;
+    const unsigned need = (unsigned)((w1 - w0) * (a.tb / a.group));
+    return ld_acquire(a.done_w + w) >= need;
+  }
   const unsigned need = (unsigned)(it.g == a.ngroups - 1 ? a.ta_last : a.ta);
   return ld_acquire(a.done_a + it.g) >= need;
 }
+
+// C-tile width: PPT positions per consumer thread (KC = PPT * NT elements)
+template <typename T, int NT>
+struct K4AbftChunk {
+  static constexpr int PPT = sizeof(T) == 4 ? 8 : 4;
+};
 
 template <typename T, int L1, int L2, bool INV, int E, int NT, int S>
 struct K4Cfg {
@@ -157,14 +183,15 @@ struct K4Cfg {
   static constexpr int BPC = (int)sizeof(C<T>);
   static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));  // shared twiddle tables
   static constexpr int RR = 4;  // release ring depth (consumer -> releaser warp)
-  static constexpr int SMEM = (SLOTS + S * TILE + TWE) * BPC + S * 16 + S * 8 + RR * 24 + 128;
+  static constexpr int REDB = 2 * (NT / 32) * 5 * 8;  // fused ABFT: C-tile warp partials, two parities
+  static constexpr int SMEM = (SLOTS + S * TILE + TWE) * BPC + S * 16 + S * 8 + RR * 24 + REDB + 128;
 };
 
 // Warp-specialised: NT consumer threads (column FFTs) + one producer warp
 // whose elected lane draws tickets, waits for the tile's dependencies and
 // lands it with 2-D TMA boxes into an S-deep staging ring ([row][column]
 // dense). Consumers never wait on scheduling, only on data.
-template <typename T, int L1, int L2, bool INV, int E, int NT, int S, int MINB>
+template <typename T, int L1, int L2, bool INV, int E, int NT, int S, int MINB, bool ABFT = false>
 __global__ void __launch_bounds__(NT + 64, MINB)
     k4_kernel(const __grid_constant__ CUtensorMap tmx, K4Args a) {
   using K = K4Cfg<T, L1, L2, INV, E, NT, S>;
@@ -222,7 +249,15 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       const long long t = rtk[i];
       if (t < 0) return;
       const K4Item c = k4_decode(a, t);
-      red_release_add(c.phase == 0 ? a.done_a + c.g : a.done_b + c.g, 1u);
+      if (c.phase == 0) {
+        red_release_add(a.done_a + c.g, 1u);
+      } else if (c.phase == 1) {
+        red_release_add(a.done_b + c.g, 1u);
+        if constexpr (ABFT) {
+          const int64_t sig = c.g * a.group + c.r / (a.tb / a.group);
+          red_release_add(a.done_w + sig / a.win, 1u);
+        }
+      }
       mbar_arrive(&relfree[i]);
     }
   }
@@ -255,7 +290,10 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       tk[s] = t;
       CT* dst = stage + s * K::TILE;
       const int r = (int)item.r;
-      if (item.phase == 0) {
+      if (item.phase == 2) {
+        // C tile: the consumers read x and y themselves (L2-hot)
+        mbar_arrive(&full[s]);
+      } else if (item.phase == 0) {
         const int sl = r / ncbA;
         const int c0 = (r - sl * ncbA) * PA::CB;
         const int row0 = (int)((item.g * G + sl) * N1);
@@ -306,7 +344,93 @@ __global__ void __launch_bounds__(NT + 64, MINB)
     const CT* st = stage + s * K::TILE;
     CT v[E];
     const int r = (int)cur.r;
-    if (cur.phase == 0) {
+    if (ABFT && cur.phase == 2) {
+      // ---- C tile (fused two-sided ABFT): window w, positions [k0, k0 + KC)
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+      constexpr int PPT = K4AbftChunk<T, NT>::PPT;  // positions per thread
+      constexpr int KC = PPT * NT;
+      constexpr int NW = NT / 32;
+      const int64_t gw = a.group / a.win;
+      const int64_t w = cur.g * gw + r / a.nchunk;
+      const int64_t ch = r % a.nchunk;
+      const int64_t w0 = w * a.win, w1 = min(w0 + a.win, a.batch);
+      const int64_t k0 = ch * KC;
+      const CT* __restrict__ xs = static_cast<const CT*>(a.x);
+      const CT* __restrict__ rowp = static_cast<const CT*>(a.row);
+      double* red = reinterpret_cast<double*>(rtk + K::RR);
+      CT rv[PPT], si[PPT], so[PPT], ev[PPT], cx[PPT], cy[PPT];
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
+        const int64_t k = k0 + tid + NT * i;
+        rv[i] = __ldg(rowp + k);
+        si[i] = so[i] = mk<T>(0, 0);
+        if (a.enc == ENC_ONES) {
+          ev[i] = mk<T>(1, 0);
+        } else {  // wang: omega_3^(k mod 3) (abft.py:93-94)
+          const int m = (int)(k % 3);
+          const T h = (T)0.86602540378443864676372317075294;
+          ev[i] = m == 0 ? mk<T>(1, 0) : (m == 1 ? mk<T>((T)-0.5, -h) : mk<T>((T)-0.5, h));
+        }
+        cx[i] = xs[w0 * N + k];
+        cy[i] = y[w0 * N + k];
+      }
+#pragma unroll 1
+      for (int64_t j = w0; j < w1; ++j) {
+        CT nx[PPT], ny[PPT];
+        if (j + 1 < w1) {  // next signal's loads in flight while this one is reduced
+#pragma unroll
+          for (int i = 0; i < PPT; ++i) {
+            const int64_t k = k0 + tid + NT * i;
+            nx[i] = xs[(j + 1) * N + k];
+            ny[i] = y[(j + 1) * N + k];
+          }
+        }
+        const T wj = (T)(a.weight0 + j + 1);
+        T r5[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) {
+          r5[0] = rfma(rv[i].x, cx[i].x, rfma(-rv[i].y, cx[i].y, r5[0]));
+          r5[1] = rfma(rv[i].x, cx[i].y, rfma(rv[i].y, cx[i].x, r5[1]));
+          r5[2] = rfma(cx[i].x, cx[i].x, rfma(cx[i].y, cx[i].y, r5[2]));
+          r5[3] = rfma(ev[i].x, cy[i].x, rfma(-ev[i].y, cy[i].y, r5[3]));
+          r5[4] = rfma(ev[i].x, cy[i].y, rfma(ev[i].y, cy[i].x, r5[4]));
+          si[i] = mk<T>(rfma(wj, cx[i].x, si[i].x), rfma(wj, cx[i].y, si[i].y));
+          so[i] = mk<T>(rfma(wj, cy[i].x, so[i].x), rfma(wj, cy[i].y, so[i].y));
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) r5[q] = radd(r5[q], __shfl_xor_sync(0xffffffffu, r5[q], off));
+        const int par = (int)(j & 1);  // two buffers: a warp may run one signal ahead
+        if ((tid & 31) == 0)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) red[(par * NW + (tid >> 5)) * 5 + q] = (double)r5[q];
+        fft_sync<NT>();
+        if (tid < 5) {  // the chunk's partial of signal j, warps in order
+          double acc = red[(par * NW) * 5 + tid];
+#pragma unroll
+          for (int ww = 1; ww < NW; ++ww) acc += red[(par * NW + ww) * 5 + tid];
+          a.sig_part[(j * a.nchunk + ch) * 5 + tid] = acc;
+        }
+        if (j + 1 < w1) {
+#pragma unroll
+          for (int i = 0; i < PPT; ++i) {
+            cx[i] = nx[i];
+            cy[i] = ny[i];
+          }
+        }
+      }
+      CT* sin_ = static_cast<CT*>(a.s_in) + w * N;
+      CT* sout_ = static_cast<CT*>(a.s_out) + w * N;
+#pragma unroll
+      for (int i = 0; i < PPT; ++i) {
+        const int64_t k = k0 + tid + NT * i;
+        sin_[k] = si[i];
+        sout_[k] = so[i];
+      }
+      fft_sync<NT>();  // red[] and the slots are free again
+    } else if (cur.phase == 0) {
       using P = PA;
 #pragma unroll
       for (int k = 0; k < E; ++k) v[k] = st[(tA + P::TPS * k) * P::CB + gA];
@@ -383,7 +507,9 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       for (int k = 0; k < E; ++k) {
         CT val = v[k];
         if constexpr (INV) val = cscale<T>(val, (T)(1.0 / (double)N));
-        __stcs(d + (int64_t)(tB + P::TPS * P::F::out_pos(k)) * N1, val);
+        // ABFT: plain stores keep y in L2 for the window's C tiles
+        if constexpr (ABFT) d[(int64_t)(tB + P::TPS * P::F::out_pos(k)) * N1] = val;
+        else __stcs(d + (int64_t)(tB + P::TPS * P::F::out_pos(k)) * N1, val);
       }
     }
     __syncwarp();
@@ -413,6 +539,37 @@ static int launch_k4_t(const K4Args& a, int num_sms, cudaStream_t st) {
   if (grid > total) grid = total;
   if (grid < 1) return 0;
   // tensor map: x as (B*N1) rows of N2 complex
+  CUtensorMap tmx;
+  const int bpc = (int)sizeof(C<T>);
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  int rc = k4_encode_2d(&tmx, dt, const_cast<void*>(a.x), (uint64_t)(2 << L2), (uint64_t)a.batch << L1,
+                        (uint64_t)bpc << L2, (uint32_t)(2 * K::PA::CB), (uint32_t)K::PA::BOXR);
+  if (rc) return rc;
+  kern<<<(unsigned)grid, NT + 64, K::SMEM, st>>>(tmx, a);
+  return (int)cudaGetLastError();
+}
+
+// fused-ABFT K4 (forward only): the same tiles plus the C tiles
+template <typename T, int L1, int L2, int E, int NT, int S, int MINB>
+static int launch_k4_abft_t(const K4Args& a, int num_sms, cudaStream_t st) {
+  using K = K4Cfg<T, L1, L2, false, E, NT, S>;
+  auto kern = k4_kernel<T, L1, L2, false, E, NT, S, MINB, true>;
+  static LaunchCfg cfg;
+  const int dev = current_device();
+  if (!cfg.done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    int ps = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, NT + 64, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    cfg.per_sm[dev] = ps < 1 ? 1 : ps;
+    cfg.done[dev] = true;
+  }
+  const int64_t total =
+      (a.ngroups - 1) * (a.ta + a.tb + a.tc) + a.ta_last + a.tb_last + a.tc_last;
+  int64_t grid = (int64_t)num_sms * cfg.per_sm[dev];
+  if (grid > total) grid = total;
+  if (grid < 1) return 0;
   CUtensorMap tmx;
   const int bpc = (int)sizeof(C<T>);
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
@@ -839,6 +996,29 @@ bool k4_supported(int prec, int l1, int l2) {
 #undef TFFT_K4
   if (!inst) return false;
   return prec == 0 ? k4_shape_ok<float>(l1, l2) : k4_shape_ok<double>(l1, l2);
+}
+
+template <typename T>
+static int dispatch_k4_abft(int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
+#define TFFT_K4(A, B)                                                                                   \
+  if (l1 == A && l2 == B) {                                                                             \
+    using SH = K4Shape<T, (A > B ? A : B)>;                                                             \
+    return launch_k4_abft_t<T, A, B, SH::E, SH::NT, SH::S, SH::MINB>(a, num_sms, st);                   \
+  }
+  TFFT_K4_PAIRS
+#undef TFFT_K4
+  return (int)cudaErrorInvalidValue;
+}
+
+int k4_abft_chunk(int prec, int l1, int l2) {
+  const int lmax = l1 > l2 ? l1 : l2;
+  if (prec == 0) return K4AbftChunk<float, 8>::PPT * (lmax <= 8 ? K4Shape<float, 8>::NT : K4Shape<float, 11>::NT);
+  return K4AbftChunk<double, 8>::PPT * K4Shape<double, 8>::NT;
+}
+
+int launch_k4_abft(int prec, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
+  if (prec == 0) return dispatch_k4_abft<float>(l1, l2, a, num_sms, st);
+  return dispatch_k4_abft<double>(l1, l2, a, num_sms, st);
 }
 
 int launch_k4(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {

@@ -37,11 +37,30 @@ struct K4Args {
   unsigned long long* ticket;  // zeroed before the launch
   unsigned* done_a;      // [ngroups] finished pass-A tiles, zeroed before the launch
   unsigned* done_b;      // [ngroups]
+  // ---- fused two-sided ABFT (K4 only; abft = 0: plain transform). After the
+  // B tiles of each group come its C tiles: (window, position chunk) items
+  // that read x and y of the window's signals while they are still in L2 and
+  // form the window sums s_in / s_out (complete: G % win == 0) and per
+  // (signal, chunk) checksum partials (abft.py:648-665, :592-624).
+  int abft;
+  int enc;               // ENC_WANG / ENC_ONES
+  int64_t win;           // W = T * bs signals per verification window
+  int64_t tc, tc_last;   // C tiles of a full / the last group
+  int64_t nchunk;        // position chunks per signal (one C tile each)
+  int64_t weight0;       // global index of row 0 (location weights weight0 + j + 1)
+  const void* row;       // left checksum row (working precision)
+  void* s_in;            // [nwin][N]
+  void* s_out;           // [nwin][N]
+  double* sig_part;      // [B][nchunk][5]
+  unsigned* done_w;      // [nwin] finished B tiles per window, zeroed before the launch
 };
 
 bool k4_supported(int prec, int l1, int l2);
 int k4_columns_per_tile(int prec, int logl, int lmax);
 int launch_k4(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
+// fused-ABFT K4 (forward): C-tile chunk width in elements and consumer warps
+int k4_abft_chunk(int prec, int l1, int l2);
+int launch_k4_abft(int prec, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
 // K7: FP64 K4 variant with warp-local columns (columns <= 512 points); the
 // intermediate ring is p-major instead of K4's column-blocked layout
 bool k7_supported(int l1, int l2);
