@@ -86,6 +86,12 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
                      int64_t bs, tfft_plan** out);
 int tfft_plan_destroy(tfft_plan* plan);
 
+/* Debug hook of the CLI self-test (reference cli.py:254-264 `_skew_plan`):
+ * multiplies the plan's w_N^1 twiddle (forward and inverse tables) by
+ * (1 + 1e-3) so the oracle and checksum checks must fail. Never used by a
+ * transform; destroy the plan afterwards. */
+int tfft_debug_skew_twiddle(tfft_plan* plan);
+
 /* Plain transform of `batch` rows, out of place; replaces execute_plan's
  * transaction loop (fft_core.py:296-329) and _run_transaction (:255-280),
  * including armed fault strikes and inverse x 1/N. `signal_offset` is the

@@ -44,6 +44,7 @@ SIGNATURES = {
     "tfft_plan_create": (c_int, [c_i64, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_i32), c_i64,
                                  ctypes.POINTER(c_vp)]),
     "tfft_plan_destroy": (c_int, [c_vp]),
+    "tfft_debug_skew_twiddle": (c_int, [c_vp]),
     "tfft_execute": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_i64, ctypes.POINTER(TfftFault), c_int, c_vp, c_vp]),
     "tfft_protected": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_dbl, c_i64, ctypes.POINTER(TfftFault),
                                c_int, ctypes.POINTER(TfftSums), c_vp, c_vp]),

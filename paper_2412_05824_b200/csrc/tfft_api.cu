@@ -489,6 +489,27 @@ int tfft_plan_destroy(tfft_plan* p) {
   return TFFT_OK;
 }
 
+int tfft_debug_skew_twiddle(tfft_plan* p) {
+  if (!p) return fail(TFFT_EINVAL, "null plan");
+  if (!p->k1 || p->n < 2) return fail(TFFT_EUNSUPPORTED, "skew hook: single-pass plans only");
+  for (DevBuf* b : {&p->tw_fwd, &p->tw_inv}) {
+    if (p->prec == 0) {
+      float v[2];
+      TFFT_TRY((int)cudaMemcpy(v, (float*)b->p + 2, sizeof(v), cudaMemcpyDeviceToHost), "skew read");
+      v[0] *= 1.001f;
+      v[1] *= 1.001f;
+      TFFT_TRY((int)cudaMemcpy((float*)b->p + 2, v, sizeof(v), cudaMemcpyHostToDevice), "skew write");
+    } else {
+      double v[2];
+      TFFT_TRY((int)cudaMemcpy(v, (double*)b->p + 2, sizeof(v), cudaMemcpyDeviceToHost), "skew read");
+      v[0] *= 1.001;
+      v[1] *= 1.001;
+      TFFT_TRY((int)cudaMemcpy((double*)b->p + 2, v, sizeof(v), cudaMemcpyHostToDevice), "skew write");
+    }
+  }
+  return TFFT_OK;
+}
+
 int tfft_execute(tfft_plan* p, const void* x, void* y, int64_t batch, int inverse, int64_t signal_offset,
                  const tfft_fault* faults, int nfaults, uint64_t* counters, void* stream) {
   if (!p || !x || !y || batch < 1) return fail(TFFT_EINVAL, "invalid execute arguments");

@@ -20,7 +20,7 @@ import types
 import pytest
 
 import paper_2412_05824_b200 as pkg
-from paper_2412_05824_b200 import abft, backend, fault, fft_core, plan, signal_io
+from paper_2412_05824_b200 import abft, backend, cli, fault, fft_core, plan, signal_io
 
 from oracle import ref_oracle
 
@@ -38,7 +38,7 @@ def _install_alias():
         setattr(mod, fn, getattr(ref_oracle, fn))
     mod.dft_oracle = oracle_mod
     sys.modules["resilient_fft"] = mod
-    for name, m in (("abft", abft), ("backend", backend), ("fault", fault), ("fft_core", fft_core),
+    for name, m in (("abft", abft), ("backend", backend), ("cli", cli), ("fault", fault), ("fft_core", fft_core),
                     ("plan", plan), ("signal_io", signal_io), ("dft_oracle", oracle_mod)):
         sys.modules[f"resilient_fft.{name}"] = m
         setattr(mod, name, m)
@@ -47,6 +47,8 @@ def _install_alias():
 _install_alias()
 
 DESELECTED = {
+    "test_module_entry_point": "runs `python -m resilient_fft` in a fresh interpreter, where the alias does not "
+                               "exist; tests/test_cli_gpu.py runs `python -m paper_2412_05824_b200 selftest --quick`",
     "test_backend_selection_and_errors": "selects the numpy 'python' backend; no CPU fallback by design",
     "test_backend_env_override": "forces RESILIENT_FFT_BACKEND=python; no CPU fallback by design",
 }

@@ -18,7 +18,7 @@ from pathlib import Path
 SRC = Path("/root/reference/pkg/tests")
 DST = Path(__file__).resolve().parent
 FILES = ["test_backends.py", "test_fft_core.py", "test_abft.py", "test_fault.py", "test_plan.py",
-         "test_acceptance.py"]
+         "test_acceptance.py", "test_cli.py"]
 
 if __name__ == "__main__":
     for f in FILES:
