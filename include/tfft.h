@@ -133,6 +133,21 @@ int tfft_group_divergence(int precision, const void* ref, const void* s_out, int
  * precision plans (abft.py:297-317); res_dev[0] = all finite, [1] = max|col|. */
 int tfft_correction_column(tfft_plan* plan, const void* snap_in, const void* snap_out, double weight, void* col,
                            double* res_dev, void* stream);
+/* Batched online correction of windows holding exactly one triggered signal
+ * (abft.py:392-418 + :493-551, the replay's common case, all items at once):
+ * item i has desc_host[6i..6i+5] = {k, r0, r1, w, w0, w1} (local rows: the
+ * signal, its transaction [r0, r1), its window index and rows [w0, w1)) and
+ * par_host[4i..4i+3] = {weight w_k, floor_k, Re c_in_k, Im c_in_k}. For each:
+ * t_in / t_out of the transaction, col = (t_out - FFT(t_in)) / w_k (FFT in FP64
+ * for single precision), usable = finite && max|col| <= 16 log2N floor sqrt N;
+ * when usable and the re-verify detect(c_in, (y_k - col) . enc) holds, y_k -=
+ * col and the window's s_out -= w_k col; then the window's group divergence.
+ * out_host[4i..4i+3] = {corrected (1/0), re-verify divergence, group divergence,
+ * max|col|}. y is untouched for items not corrected. Window sums come from the
+ * last tfft_protected call on this plan when it kept them. Synchronous. */
+int tfft_correct_windows(tfft_plan* plan, const void* x, void* y, int64_t signal_offset, int64_t count,
+                         const int64_t* desc_host, const double* par_host, int enc_kind, double delta,
+                         double* out_host, void* stream);
 /* y_row -= col; res_dev[2..3] = y_row . enc (abft.py:404-406) */
 int tfft_patch_row(tfft_plan* plan, void* y_row, const void* col, int enc_kind, double* res_dev, void* stream);
 /* per-row checksums for rows [row0, row0+nrows) of x/y into `sums`

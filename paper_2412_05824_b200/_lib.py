@@ -56,6 +56,8 @@ SIGNATURES = {
     "tfft_group_divergence": (c_int, [c_int, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "tfft_correction_column": (c_int, [c_vp, c_vp, c_vp, c_dbl, c_vp, c_vp, c_vp]),
     "tfft_patch_row": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
+    "tfft_correct_windows": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl),
+                                     c_int, c_dbl, ctypes.POINTER(c_dbl), c_vp]),
     "tfft_row_checksums": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_dbl, ctypes.POINTER(TfftSums), c_vp,
                                    c_int, c_vp]),
     "tfft_jou_variant": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),

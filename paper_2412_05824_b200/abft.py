@@ -20,6 +20,7 @@ Where the work happens:
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from functools import lru_cache
 
@@ -33,6 +34,7 @@ from .fft_core import (
     PRECISIONS,
     REAL_DTYPES,
     SignalBatch,
+    Transaction,
     _check_plan_batch,
     _Counters,
     _output,
@@ -276,9 +278,10 @@ class _DeviceSums:
         return fft_core._Counters.decode(h[:4].view(np.int64)), h[4:]
 
     def host(self):
-        c_in = self.c_in.cpu().numpy().view(np.complex128)
-        c_out = self.c_out.cpu().numpy().view(np.complex128)
-        return c_in, c_out, self.floors.cpu().numpy(), self.div.cpu().numpy()
+        """(c_in, c_out, floors, div) on the host, in one device-to-host copy."""
+        h = self.buf[4 + self.nwin:].cpu().numpy()
+        b = h.size // 6
+        return (h[:2 * b].view(np.complex128), h[2 * b:4 * b].view(np.complex128), h[4 * b:5 * b], h[5 * b:])
 
 
 def _weighted_columns(plan, src, row0, row1, group, weight0=0):
@@ -426,6 +429,23 @@ class _ProtectedRun:
             self._handle_detections(tx, t_in, t_out, triggered, tx_by_index)
         if state.transactions_seen % state.group_size == 0:
             self._verify(tx_by_index)
+
+    def batched_window(self, ntx, tx, k, div, decoded, group_div):
+        """A window corrected by _batched_windows: the events, counters and
+        report the serial replay produces for one trigger whose correction
+        holds (abft.py:422-551: event, pending, patch + re-verify, decontaminated
+        verification)."""
+        self.state.transactions_seen += ntx
+        event = DetectionEvent(tx.index + self.tx_off, k + self.sig_off, div, decoded)
+        self.stats.events.append(event)
+        self.stats.corrections += 1
+        group_hit = group_div > self.delta
+        divergence = max([div] + ([group_div] if group_hit else []))
+        self.stats.verifications += 1
+        self.state.verifications += 1
+        self.reports.append(DetectionReport(triggered=True, divergence=float(divergence), located=k + self.sig_off,
+                                            corrected=True, uncorrectable=False,
+                                            verification_index=self.state.verifications - 1))
 
     def skip_clean_window(self, ntx, group_div):
         """A window without triggers: same report the replay would produce."""
@@ -639,24 +659,114 @@ def _protected(plan, batch, e_left, delta, group_size, mode, injector, stats, ou
     else:
         host = sums.host()
         run = _ProtectedRun(plan, source, y, delta, group_size, kind, stats, host, sig_off, global_b)
-        txs = transaction_partition(plan, batch)
-        tx_by_index = {tx.index: tx for tx in txs}
+        txs = _TxTable(plan.bs, batch.b)
+        tx_by_index = txs
         div = host[3]
+        batched = _batched_windows(plan, source, y, batch, txs, ntx, nwin, group_size, div, host, kind, delta,
+                                   sig_off, run)
+        win_hit = np.zeros(nwin, dtype=bool)
+        win_hit[(np.flatnonzero(div > delta) // plan.bs) // group_size] = True
         with np.errstate(over="ignore", invalid="ignore"):
             for w in range(nwin):
                 first, last = w * group_size, min((w + 1) * group_size, ntx)
-                a, b = txs[first].start, txs[last - 1].stop
-                if not _FORCE_ENGINE and not bool((div[a:b] > delta).any()):
+                if not _FORCE_ENGINE and not win_hit[w]:
                     run.skip_clean_window(last - first, float(win_div[w]))
+                    continue
+                a, b = txs[first].start, txs[last - 1].stop
+                if w in batched:
+                    run.batched_window(last - first, *batched[w])
                     continue
                 t_in = _weighted_columns(plan, source, a, b, plan.bs, sig_off)
                 t_out = _weighted_columns(plan, y, a, b, plan.bs, sig_off)
-                for i, tx in enumerate(txs[first:last]):
-                    run.feed(tx, t_in[i], t_out[i], tx_by_index)
+                for i, ti in enumerate(range(first, last)):
+                    run.feed(txs[ti], t_in[i], t_out[i], tx_by_index)
             reports = run.finish(tx_by_index)
     if kind == "jou":
         _jou_undo_dev(plan, y)
     return _output(batch, y, out), reports
+
+
+class _TxTable:
+    """transaction_partition's entries made on demand (fft_core.py:245-252):
+    a triggered run touches a few of the ntx transactions, and building all
+    of them costs ~1 us each on the host."""
+
+    def __init__(self, bs, b):
+        self.bs, self.b = bs, b
+
+    def __getitem__(self, i):
+        start = i * self.bs
+        return Transaction(i, start, min(start + self.bs, self.b))
+
+
+def _batched_windows(plan, source, y, batch, txs, ntx, nwin, T, div, host, kind, delta, sig_off, run):
+    """The replay's common case for all windows at once (tfft_correct_windows):
+    windows whose only trigger is one signal are corrected in one batched
+    call -- snapshot sums, FP64 correction FFTs, usability, patch, re-verify,
+    decontaminated window check -- instead of per-event host round trips.
+    Returns {window: (tx, signal, divergence, decoded, group_div)} for the
+    windows it corrected; every other triggered window (several triggers,
+    an unusable column, a failed re-verify) goes through the serial replay,
+    with y untouched by this call, so decisions stay the reference's."""
+    if _FORCE_ENGINE or kind not in ("wang", "ones") or os.environ.get("TFFT_NO_BATCHED_CORRECTION"):
+        return {}
+    hits = np.flatnonzero(div > delta)
+    if hits.size == 0:
+        return {}
+    bs = plan.bs
+    win_of = (hits // bs) // T
+    wins, first_idx, counts = np.unique(win_of, return_index=True, return_counts=True)
+    sel = counts == 1
+    if not sel.any():
+        return {}
+    wsel = wins[sel]
+    k = hits[first_idx[sel]]
+    c_in, c_out, floors = host[0], host[1], host[2]
+    b = batch.b
+    r0 = (k // bs) * bs
+    r1 = np.minimum(r0 + bs, b)
+    w0 = wsel * T * bs
+    w1 = np.minimum((wsel + 1) * T * bs, b)
+    desc = np.ascontiguousarray(np.stack([k, r0, r1, wsel, w0, w1], axis=1).astype(np.int64))
+    weights = np.asarray(run.state.weights)
+    par = np.ascontiguousarray(np.stack([weights[k].astype(np.float64), np.maximum(floors[k], DIVERGENCE_FLOOR),
+                                         c_in[k].real, c_in[k].imag], axis=1).astype(np.float64))
+    count = int(k.size)
+    out = np.zeros(4 * count, dtype=np.float64)
+    lib = _lib.load()
+    rc = lib.tfft_correct_windows(plan.native, source.data_ptr(), y.data_ptr(), int(sig_off), count,
+                                  desc.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  par.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _lib.ENC[kind], float(delta),
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _device.stream_handle())
+    _lib.check(rc, "tfft_correct_windows")
+    meta = [(int(wsel[i]), txs[int(k[i]) // bs], int(k[i])) for i in range(count)]
+    res = {}
+    ok = out.reshape(count, 4)
+    done = [int(i) for i in np.flatnonzero(ok[:, 0] == 1.0)]  # others: the serial replay handles the window
+    if not done:
+        return res
+    # the transaction residual sums of _handle_detections (abft.py:463-466),
+    # same sequential order, vectorised across the windows
+    weights = np.asarray(run.state.weights, dtype=np.float64)
+    starts = np.array([meta[i][1].start for i in done])
+    sizes = np.array([meta[i][1].stop - meta[i][1].start for i in done])
+    tx_res = np.zeros(len(done), dtype=np.complex128)
+    tx_wres = np.zeros(len(done), dtype=np.complex128)
+    with np.errstate(over="ignore", invalid="ignore"):
+        for j in range(int(sizes.max())):
+            live = j < sizes
+            idx = np.where(live, starts + j, starts)
+            r = np.where(live, c_in[idx] - c_out[idx], 0)
+            tx_res = tx_res + r
+            tx_wres = tx_wres + np.where(live, weights[idx], 0.0) * r
+        for q, i in enumerate(done):
+            w, tx, k = meta[i]
+            try:
+                decoded = locate(complex(tx_wres[q]), complex(tx_res[q]), batch=run.global_b) - 1
+            except Undecodable:
+                decoded = None
+            res[w] = (tx, k, float(div[k]), decoded, float(ok[i, 2]))
+    return res
 
 
 def run_offline(plan, batch, e_left="wang", delta=None, *, workers=1, injector=None, stats=None, out=None):

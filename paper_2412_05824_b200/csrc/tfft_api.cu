@@ -137,6 +137,10 @@ struct tfft_plan {
   DevBuf faults;
   DevBuf ws, win_count;
   DevBuf sigpart;                     // K5 fused ABFT: per-warp per-signal partials
+  DevBuf winsave;                     // K5 fused ABFT: the last call's window sums [nwin][2][n]
+  int sums_kind = 0;                  // window sums of the last protected call: 0 none, 1 winsave, 2 wsum
+  int64_t sums_nwin = 0;
+  DevBuf cw_desc, cw_par, cw_res, cw_tin, cw_tout, cw_ref, cw_col, cw_sin, cw_sout, cw_gref;  // batched correction
   DevBuf scratch_a, scratch_b, base;  // strike path
   DevBuf col_a, col_b, col64;         // single-column work
   K3Plan* k3 = nullptr;               // two-pass machinery (N beyond K1)
@@ -283,8 +287,10 @@ int split_faults(tfft_plan* p, const tfft_fault* faults, int nfaults, int64_t si
   return 0;
 }
 
-int upload_faults(tfft_plan* p, const std::vector<DevFault>& dev, cudaStream_t st) {
+int upload_faults(tfft_plan* p, std::vector<DevFault>& dev, cudaStream_t st) {
   if (dev.empty()) return 0;
+  // sorted by signal (stable: same-signal faults keep their order) for fault_lo
+  std::stable_sort(dev.begin(), dev.end(), [](const DevFault& a, const DevFault& b) { return a.signal < b.signal; });
   int e = p->faults.ensure(dev.size() * sizeof(DevFault));
   if (e) return cuda_fail(e, "fault buffer");
   TFFT_TRY((int)cudaMemcpyAsync(p->faults.p, dev.data(), dev.size() * sizeof(DevFault), cudaMemcpyHostToDevice, st),
@@ -479,7 +485,8 @@ int tfft_plan_create(int64_t n, int precision, int nstages, const int64_t* spans
 
 int tfft_plan_destroy(tfft_plan* p) {
   if (!p) return TFFT_OK;
-  DevBuf* all[] = {&p->sigpart, &p->part, &p->tw_fwd, &p->tw_inv, &p->enc_tab[0], &p->enc_tab[1], &p->wsum, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
+  DevBuf* all[] = {&p->winsave, &p->cw_desc, &p->cw_par, &p->cw_res, &p->cw_tin, &p->cw_tout, &p->cw_ref,
+                   &p->cw_col, &p->cw_sin, &p->cw_sout, &p->cw_gref, &p->sigpart, &p->part, &p->tw_fwd, &p->tw_inv, &p->enc_tab[0], &p->enc_tab[1], &p->wsum, &p->rows[0], &p->rows[1], &p->rows[2], &p->counters, &p->faults,
                    &p->ws, &p->win_count, &p->scratch_a, &p->scratch_b, &p->base, &p->col_a, &p->col_b, &p->col64};
   for (DevBuf* b : all) b->release();
   if (p->k3) k3_destroy(p->k3);
@@ -574,7 +581,10 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     const size_t cb = cbytes(p->prec);
     e = p->ws.ensure((size_t)grid * maxseg * spt * 2 * p->n * cb);
     if (!e) e = p->sigpart.ensure((size_t)batch * nws * 5 * sizeof(double));
+    if (!e) e = p->winsave.ensure((size_t)nwin * 2 * p->n * cb);
     if (e) return cuda_fail(e, "abft workspace");
+    p->sums_kind = 1;
+    p->sums_nwin = nwin;
     ab.mode = 2;
     ab.pieces = maxseg;
     ab.ws = p->ws.p;
@@ -591,9 +601,11 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     a.abft = ab;
     TFFT_TRY(launch_k5_abft(p->prec, p->logn, a, p->num_sms, st), "k5 abft launch");
     TFFT_TRY(launch_k5_window_finish(p->prec, p->logn, p->ws.p, (const double*)p->sigpart.p, nws, p->tw_fwd.p, batch,
-                                     W, grid, maxseg, spt, nwin, delta, ab, (Counters*)counters, p->num_sms, st),
+                                     W, grid, maxseg, spt, nwin, delta, ab, (Counters*)counters, p->winsave.p,
+                                     p->num_sms, st),
              "abft window finish");
   } else if (p->k1 && !sweep) {
+    p->sums_kind = 0;
     const int spt = k1_slots(p->prec, p->logn);
     if (W <= 4) {
       ab.mode = 0;
@@ -651,6 +663,8 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
                             st);
       if (rk != (int)cudaErrorNotSupported) {
         if (rk) return cuda_fail(rk, "fused k4 abft launch");
+        p->sums_kind = 2;
+        p->sums_nwin = nwin;
         g_launches.fetch_add(1, std::memory_order_relaxed);
         TFFT_TRY(launch_signal_epilogue((const double*)p->sigpart.p, nparts, p->n, batch, delta, ab,
                                         (Counters*)counters, st),
@@ -683,6 +697,8 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     TFFT_TRY(launch_window_sweep(p->prec, x, y, p->n, batch, W, signal_offset, p->rows[enc].p, etab,
                                  enc, s_in, s_out, (double*)p->part.p, ab, delta, (Counters*)counters, st),
              "abft sweep");
+    p->sums_kind = slow.empty() ? 2 : 0;  // strike-path rows changed after the sweep: recompute sums
+    p->sums_nwin = nwin;
     std::vector<DevFault> none;
     int e2 = p->counters.ensure(8 * sizeof(uint64_t));
     if (e2) return cuda_fail(e2, "counters");
@@ -694,6 +710,7 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     return TFFT_OK;
   }
   if (slow.empty()) return TFFT_OK;
+  p->sums_kind = 0;  // y changes below: kept window sums no longer match it
   // strike path for the faults the fused kernel cannot reach, then refresh
   // the affected rows' checksums and their windows' group divergences
   std::vector<int64_t> touched;
@@ -829,6 +846,101 @@ int tfft_correction_column(tfft_plan* p, const void* snap_in, const void* snap_o
   if (rc) return rc;
   TFFT_TRY(launch_correction_column(p->prec, snap_out, p64->col_a.p, p->n, weight, col, res_dev, st),
            "correction column");
+  return TFFT_OK;
+}
+
+int tfft_correct_windows(tfft_plan* p, const void* x, void* y, int64_t signal_offset, int64_t count,
+                         const int64_t* desc_host, const double* par_host, int enc, double delta, double* out_host,
+                         void* stream) {
+  if (!p || !x || !y || count < 0 || (count && (!desc_host || !par_host || !out_host)))
+    return fail(TFFT_EINVAL, "invalid correct_windows arguments");
+  if (count == 0) return TFFT_OK;
+  if (enc != ENC_WANG && enc != ENC_ONES) return fail(TFFT_EUNSUPPORTED, "batched correction: wang / ones only");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = p->n;
+  const size_t cb = cbytes(p->prec);
+  const size_t vec = (size_t)count * n * cb;
+  int e = p->cw_desc.ensure((size_t)count * 6 * sizeof(int64_t));
+  if (!e) e = p->cw_par.ensure((size_t)count * 5 * sizeof(double));
+  if (!e) e = p->cw_res.ensure((size_t)count * 4 * sizeof(double));
+  if (!e) e = p->cw_tin.ensure(vec);
+  if (!e) e = p->cw_tout.ensure(vec);
+  if (!e) e = p->cw_ref.ensure((size_t)count * n * 16);
+  if (!e) e = p->cw_col.ensure(vec);
+  if (!e) e = p->cw_sin.ensure(vec);
+  if (!e) e = p->cw_sout.ensure(vec);
+  if (!e) e = p->cw_gref.ensure(vec);
+  if (!e) e = p->part.ensure((size_t)count * ((n + 8191) / 8192) * 2 * sizeof(double));
+  if (!e) e = p->counters.ensure(8 * sizeof(uint64_t));
+  if (e) return cuda_fail(e, "batched correction workspace");
+  const int64_t* desc = (const int64_t*)p->cw_desc.p;
+  double* par = (double*)p->cw_par.p;
+  double* res = (double*)p->cw_res.p;
+  TFFT_TRY((int)cudaMemcpyAsync(p->cw_desc.p, desc_host, (size_t)count * 6 * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, st), "desc upload");
+  TFFT_TRY((int)cudaMemcpyAsync(p->cw_par.p, par_host, (size_t)count * 4 * sizeof(double), cudaMemcpyHostToDevice,
+                                st), "par upload");
+  // the triggering transaction's snapshot (abft.py:668-677): desc = {k, r0, r1, w, w0, w1} (local rows)
+  TFFT_TRY(launch_wsum_list(p->prec, x, n, desc, 1, 2, count, signal_offset, p->cw_tin.p, st), "t_in");
+  TFFT_TRY(launch_wsum_list(p->prec, y, n, desc, 1, 2, count, signal_offset, p->cw_tout.p, st), "t_out");
+  // the window sums: kept by the last protected call, else formed here
+  const int64_t nw = p->sums_nwin;
+  if (p->sums_kind == 1) {
+    TFFT_TRY(launch_gather_rows(p->prec, p->winsave.p, 2 * n, desc, 3, count, n, p->cw_sin.p, st), "s_in gather");
+    TFFT_TRY(launch_gather_rows(p->prec, (const char*)p->winsave.p + n * cb, 2 * n, desc, 3, count, n, p->cw_sout.p,
+                                st), "s_out gather");
+  } else if (p->sums_kind == 2) {
+    TFFT_TRY(launch_gather_rows(p->prec, p->wsum.p, n, desc, 3, count, n, p->cw_sin.p, st), "s_in gather");
+    TFFT_TRY(launch_gather_rows(p->prec, (const char*)p->wsum.p + (size_t)nw * n * cb, n, desc, 3, count, n,
+                                p->cw_sout.p, st), "s_out gather");
+  } else {
+    TFFT_TRY(launch_wsum_list(p->prec, x, n, desc, 4, 5, count, signal_offset, p->cw_sin.p, st), "s_in");
+    TFFT_TRY(launch_wsum_list(p->prec, y, n, desc, 4, 5, count, signal_offset, p->cw_sout.p, st), "s_out");
+  }
+  // FFT(t_in): FP64 for single precision (abft.py:304-314), working precision otherwise
+  std::vector<DevFault> none;
+  tfft_plan* p64 = p;
+  const void* in64 = p->cw_tin.p;
+  if (p->prec == 0) {
+    if (!p->promoted) {
+      int rc = tfft_plan_create(p->n, 1, (int)p->spans.size(), p->spans.data(), p->radices.data(), p->bs,
+                                &p->promoted);
+      if (rc) return rc;
+    }
+    p64 = p->promoted;
+    e = p->cw_gref.ensure((size_t)count * n * 16);
+    if (e) return cuda_fail(e, "promote buffer");
+    TFFT_TRY(launch_promote(p->cw_tin.p, p->cw_gref.p, count * n, st), "promote");
+    in64 = p->cw_gref.p;
+    int e2 = p64->counters.ensure(8 * sizeof(uint64_t));
+    if (e2) return cuda_fail(e2, "counters");
+  }
+  int rc = run_plain(p64, in64, p->cw_ref.p, count, 0, 0, none, (uint64_t*)p64->counters.p + 4, st);
+  if (rc) return rc;
+  const void* etab = nullptr;
+  rc = enc_table(p, false, st, &etab);
+  if (rc) return rc;
+  TFFT_TRY(launch_correct_items(p->prec, y, desc, par, count, n, p->cw_tout.p, p->cw_ref.p, p->cw_col.p, enc, etab,
+                                delta, p->cw_sout.p, (double*)p->part.p, res, st),
+           "batched correction");
+  // the windows' verification after decontamination (abft.py:502-507)
+  rc = run_plain(p, p->cw_sin.p, p->cw_gref.p, count, 0, 0, none, (uint64_t*)p->counters.p + 4, st);
+  if (rc) return rc;
+  double* gd = par + 4 * count;  // group divergences (the par tail)
+  TFFT_TRY(launch_group_div_chunked(p->prec, p->cw_gref.p, p->cw_sout.p, n, count, gd, (double*)p->part.p, st),
+           "batched group div");
+  std::vector<double> hres((size_t)count * 4), hgd(count);
+  TFFT_TRY((int)cudaMemcpyAsync(hres.data(), res, hres.size() * sizeof(double), cudaMemcpyDeviceToHost, st),
+           "result download");
+  TFFT_TRY((int)cudaMemcpyAsync(hgd.data(), gd, hgd.size() * sizeof(double), cudaMemcpyDeviceToHost, st),
+           "group div download");
+  TFFT_TRY((int)cudaStreamSynchronize(st), "batched correction sync");
+  for (int64_t i = 0; i < count; ++i) {
+    out_host[i * 4 + 0] = hres[i * 4 + 0];  // 1: corrected (usable and re-verified)
+    out_host[i * 4 + 1] = hres[i * 4 + 1];  // re-verify divergence
+    out_host[i * 4 + 2] = hgd[i];           // window group divergence after decontamination
+    out_host[i * 4 + 3] = hres[i * 4 + 3];  // max |col| (inf if non-finite)
+  }
   return TFFT_OK;
 }
 

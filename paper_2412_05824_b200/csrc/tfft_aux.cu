@@ -342,6 +342,224 @@ int launch_weighted_cols(int prec, const void* src, int64_t n, int64_t row0, int
 }
 
 // ---------------------------------------------------------------------------
+// Batched online correction of single-trigger windows (tfft_correct_windows).
+// Item i: transaction rows [r0, r1) holding the triggered signal k, window
+// rows [w0, w1), weight w = weight0 + k + 1, floor, c_in (desc / par arrays).
+
+// out[i][k] = sum_{j in [ra_i, rb_i)} (weight0 + j + 1) src[j][k]; same
+// arithmetic as weighted_cols_kernel (FP64 fma, rounded once)
+template <typename T>
+__global__ void wsum_list_kernel(const C<T>* __restrict__ src, int64_t n, const int64_t* __restrict__ desc, int lo,
+                                 int hi, int64_t weight0, C<T>* __restrict__ out) {
+  const int64_t i = blockIdx.y;
+  const int64_t ra = desc[i * 6 + lo], rb = desc[i * 6 + hi];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    double re = 0, im = 0;
+    for (int64_t j = ra; j < rb; ++j) {
+      const C<T> v = src[j * n + k];
+      const double w = (double)(weight0 + j + 1);
+      re = fma(w, (double)v.x, re);
+      im = fma(w, (double)v.y, im);
+    }
+    out[i * n + k] = mk<T>((T)re, (T)im);
+  }
+}
+
+int launch_wsum_list(int prec, const void* src, int64_t n, const int64_t* desc_dev, int lo, int hi, int64_t count,
+                     int64_t weight0, void* out, cudaStream_t st) {
+  if (count < 1) return 0;
+  unsigned bx = (unsigned)((n + 255) / 256);
+  if (bx > 64) bx = 64;
+  const dim3 grid(bx, (unsigned)count);
+  if (prec == 0)
+    wsum_list_kernel<float><<<grid, 256, 0, st>>>((const float2*)src, n, desc_dev, lo, hi, weight0, (float2*)out);
+  else
+    wsum_list_kernel<double><<<grid, 256, 0, st>>>((const double2*)src, n, desc_dev, lo, hi, weight0, (double2*)out);
+  return (int)cudaGetLastError();
+}
+
+// rows src[idx_i] (n each) -> dst[i]: gathers window sums into a batch
+template <typename T>
+__global__ void gather_rows_kernel(const C<T>* __restrict__ src, int64_t stride, const int64_t* __restrict__ desc,
+                                   int col, int64_t n, C<T>* __restrict__ dst) {
+  const int64_t i = blockIdx.y, r = desc[i * 6 + col];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    dst[i * n + k] = src[r * stride + k];
+}
+
+int launch_gather_rows(int prec, const void* src, int64_t stride, const int64_t* desc_dev, int col, int64_t count,
+                       int64_t n, void* dst, cudaStream_t st) {
+  if (count < 1) return 0;
+  unsigned bx = (unsigned)((n + 255) / 256);
+  if (bx > 64) bx = 64;
+  const dim3 grid(bx, (unsigned)count);
+  if (prec == 0)
+    gather_rows_kernel<float><<<grid, 256, 0, st>>>((const float2*)src, stride, desc_dev, col, n, (float2*)dst);
+  else
+    gather_rows_kernel<double><<<grid, 256, 0, st>>>((const double2*)src, stride, desc_dev, col, n, (double2*)dst);
+  return (int)cudaGetLastError();
+}
+
+// col_i = (t_out_i - ref_i) / w_i in FP64, cast (abft.py:297-317); chunk
+// partials {non-finite count, max|col|} per (item, chunk)
+template <typename T, typename R>
+__global__ void __launch_bounds__(256) corr_cols_kernel(const C<T>* __restrict__ tout, const R* __restrict__ ref,
+                                                        const double* __restrict__ par, int64_t n, int64_t nc,
+                                                        C<T>* __restrict__ col, double* __restrict__ part) {
+  __shared__ double sh[8 * 2];
+  const int64_t i = blockIdx.y, c = blockIdx.x;
+  const double w = par[i * 4];
+  double acc[2] = {0, 0};
+  const int64_t k0 = c * kChunk, k1 = min(k0 + kChunk, n);
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += 256) {
+    const C<T> to = tout[i * n + k];
+    const R rf = ref[i * n + k];
+    double re, im;
+    if (sizeof(T) == 4) {  // FP32 data: the column is formed in FP64
+      re = ((double)to.x - (double)rf.x) / w;
+      im = ((double)to.y - (double)rf.y) / w;
+    } else {  // FP64: working precision, divided by the weight in it
+      re = (double)(((T)to.x - (T)rf.x) / (T)w);
+      im = (double)(((T)to.y - (T)rf.y) / (T)w);
+    }
+    const C<T> v = mk<T>((T)re, (T)im);
+    col[i * n + k] = v;
+    if (!isfinite((double)v.x) || !isfinite((double)v.y)) acc[0] += 1.0;
+    else acc[1] = fmax(acc[1], hypot((double)v.x, (double)v.y));
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+    acc[1] = fmax(acc[1], __shfl_xor_sync(0xffffffffu, acc[1], off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[(threadIdx.x >> 5) * 2] = acc[0];
+    sh[(threadIdx.x >> 5) * 2 + 1] = acc[1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bad = 0, mx = 0;
+    for (int q = 0; q < 8; ++q) {
+      bad += sh[2 * q];
+      mx = fmax(mx, sh[2 * q + 1]);
+    }
+    part[(i * nc + c) * 2] = bad;
+    part[(i * nc + c) * 2 + 1] = mx;
+  }
+}
+
+// usable_i = all finite && max|col| <= 16 log2N floor sqrt(N) (abft.py:320-330)
+__global__ void corr_usable_kernel(const double* part, int64_t nc, int64_t count, const double* par, double limit_scale,
+                                   double* res) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double bad = 0, mx = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    bad += part[(i * nc + c) * 2];
+    mx = fmax(mx, part[(i * nc + c) * 2 + 1]);
+  }
+  res[i * 4 + 0] = (bad == 0 && mx <= limit_scale * par[i * 4 + 1]) ? 1.0 : 0.0;
+  res[i * 4 + 3] = bad == 0 ? mx : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// re-verify: c_out' = (y_k - col) . enc in working precision per thread,
+// chunk partials in FP64 (patch_row_kernel's arithmetic) -- y is not written
+template <typename T>
+__global__ void __launch_bounds__(256) corr_reverify_kernel(const C<T>* __restrict__ y, const C<T>* __restrict__ col,
+                                                            const int64_t* __restrict__ desc, int64_t n, int64_t nc,
+                                                            int enc, const C<T>* __restrict__ tw,
+                                                            double* __restrict__ part) {
+  __shared__ double sh[8 * 2];
+  const int64_t i = blockIdx.y, c = blockIdx.x;
+  const C<T>* yk = y + desc[i * 6] * n;
+  C<T> co = mk<T>(0, 0);
+  const int64_t k0 = c * kChunk, k1 = min(k0 + kChunk, n);
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += 256) {
+    const C<T> v = csub<T>(yk[k], col[i * n + k]);
+    co = cadd<T>(co, cmul<T>(enc_value<T>(enc, k, n, tw), v));
+  }
+  double acc[2] = {(double)co.x, (double)co.y};
+  block_sum256<2>(acc, sh);
+  if (threadIdx.x == 0) {
+    part[(i * nc + c) * 2] = acc[0];
+    part[(i * nc + c) * 2 + 1] = acc[1];
+  }
+}
+
+// detect(c_in, c_out', delta, floor) (abft.py:155-167); res[i*4+1] = divergence,
+// res[i*4+0] = 1 only when usable and the re-verify holds
+__global__ void corr_decide_kernel(const double* part, int64_t nc, int64_t count, const double* par, double delta,
+                                   double* res) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double a = 0, b = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    a += part[(i * nc + c) * 2];
+    b += part[(i * nc + c) * 2 + 1];
+  }
+  const double cr = par[i * 4 + 2], ci = par[i * 4 + 3], fl = par[i * 4 + 1];
+  double dv;
+  if (!isfinite(a) || !isfinite(b)) dv = __longlong_as_double(0x7ff0000000000000ll);
+  else dv = hypot(cr - a, ci - b) / fmax(fmax(hypot(cr, ci), fl), 1e-30);
+  res[i * 4 + 1] = dv;
+  if (!(dv <= delta)) res[i * 4 + 0] = 0.0;
+}
+
+// commit for the items that passed: y_k -= col; s_out_i -= w col (working precision)
+template <typename T>
+__global__ void corr_commit_kernel(C<T>* __restrict__ y, const C<T>* __restrict__ col, const int64_t* __restrict__ desc,
+                                   const double* __restrict__ par, const double* __restrict__ res, int64_t n,
+                                   C<T>* __restrict__ s_out) {
+  const int64_t i = blockIdx.y;
+  if (res[i * 4] != 1.0) return;
+  C<T>* yk = y + desc[i * 6] * n;
+  const T w = (T)par[i * 4];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const C<T> cv = col[i * n + k];
+    yk[k] = csub<T>(yk[k], cv);
+    const C<T> so = s_out[i * n + k];
+    s_out[i * n + k] = csub<T>(so, mk<T>(w * cv.x, w * cv.y));
+  }
+}
+
+int launch_correct_items(int prec, void* y, const int64_t* desc_dev, const double* par_dev, int64_t count, int64_t n,
+                         const void* tout, const void* ref64_or_ref, void* col, int enc, const void* tw, double delta,
+                         void* s_out, double* part, double* res_dev, cudaStream_t st) {
+  if (count < 1) return 0;
+  const int64_t nc = (n + kChunk - 1) / kChunk;
+  const dim3 g2((unsigned)nc, (unsigned)count);
+  double lg = 0;
+  for (int64_t v = n; v > 1; v >>= 1) lg += 1.0;
+  const double limit_scale = 16.0 * lg * sqrt((double)n);
+  const unsigned gb = (unsigned)((count + 127) / 128);
+  if (prec == 0) {
+    corr_cols_kernel<float, double2><<<g2, 256, 0, st>>>((const float2*)tout, (const double2*)ref64_or_ref, par_dev,
+                                                         n, nc, (float2*)col, part);
+  } else {
+    corr_cols_kernel<double, double2><<<g2, 256, 0, st>>>((const double2*)tout, (const double2*)ref64_or_ref,
+                                                          par_dev, n, nc, (double2*)col, part);
+  }
+  corr_usable_kernel<<<gb, 128, 0, st>>>(part, nc, count, par_dev, limit_scale, res_dev);
+  if (prec == 0)
+    corr_reverify_kernel<float><<<g2, 256, 0, st>>>((const float2*)y, (const float2*)col, desc_dev, n, nc, enc,
+                                                    (const float2*)tw, part);
+  else
+    corr_reverify_kernel<double><<<g2, 256, 0, st>>>((const double2*)y, (const double2*)col, desc_dev, n, nc, enc,
+                                                     (const double2*)tw, part);
+  corr_decide_kernel<<<gb, 128, 0, st>>>(part, nc, count, par_dev, delta, res_dev);
+  unsigned bx = (unsigned)((n + 255) / 256);
+  if (bx > 64) bx = 64;
+  const dim3 g3(bx, (unsigned)count);
+  if (prec == 0)
+    corr_commit_kernel<float><<<g3, 256, 0, st>>>((float2*)y, (const float2*)col, desc_dev, par_dev, res_dev, n,
+                                                  (float2*)s_out);
+  else
+    corr_commit_kernel<double><<<g3, 256, 0, st>>>((double2*)y, (const double2*)col, desc_dev, par_dev, res_dev, n,
+                                                   (double2*)s_out);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // one-sweep ABFT sums for the two-pass sizes: a CTA owns (window w, chunk of
 // CH = 256 * V = 1024 (FP32) / 512 (FP64) elements) and walks the window's signals once, reading x and y
 // exactly once per element. It accumulates the window sums s_in / s_out for

@@ -29,6 +29,13 @@ int launch_window_sweep(int prec, const void* x, const void* y, int64_t n, int64
 // (summed in a fixed order), counting triggers and the max divergence
 int launch_signal_epilogue(const double* part, int64_t nparts, int64_t n, int64_t batch, double delta,
                            const AbftArgs& ab, Counters* counters, cudaStream_t st);
+int launch_wsum_list(int prec, const void* src, int64_t n, const int64_t* desc_dev, int lo, int hi, int64_t count,
+                     int64_t weight0, void* out, cudaStream_t st);
+int launch_gather_rows(int prec, const void* src, int64_t stride, const int64_t* desc_dev, int col, int64_t count,
+                       int64_t n, void* dst, cudaStream_t st);
+int launch_correct_items(int prec, void* y, const int64_t* desc_dev, const double* par_dev, int64_t count, int64_t n,
+                         const void* tout, const void* ref64_or_ref, void* col, int enc, const void* tw, double delta,
+                         void* s_out, double* part, double* res_dev, cudaStream_t st);
 int launch_seg_combine(int prec, const void* ws, int64_t n, int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt,
                        int64_t nwin, void* s_in, void* s_out, cudaStream_t st);
 // group divergence of `count` long rows through chunk partials (part: count * ceil(n / 8192) * 2 doubles)

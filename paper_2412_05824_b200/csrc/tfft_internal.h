@@ -17,6 +17,20 @@ struct DevFault {
   int32_t pad;
 };
 
+// Fault lists are uploaded sorted by signal (upload_faults): the first entry
+// of `sig` by binary search, so a kernel tile costs O(log nfaults) per
+// signal instead of a scan of every armed fault (one fault per window at C3
+// is 128 faults per launch).
+__host__ __device__ __forceinline__ int fault_lo(const DevFault* f, int n, int64_t sig) {
+  int a = 0, b = n;
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (f[m].signal < sig) a = m + 1;
+    else b = m;
+  }
+  return a;
+}
+
 enum EncKind : int { ENC_WANG = 0, ENC_ONES = 1, ENC_JOU = 2 };
 
 // status words (device): [0] non-finite input seen, [1] triggered signals,
@@ -72,7 +86,7 @@ int launch_k5_abft(int prec, int logn, const K1Args& a, int num_sms, cudaStream_
 int k5_abft_layout(int prec, int logn, int num_sms, int64_t batch, int64_t* grid, int* spt, int* nws);
 int launch_k5_window_finish(int prec, int logn, const void* ws, const double* sig_part, int nws, const void* tw,
                             int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta,
-                            const AbftArgs& ab, Counters* counters, int num_sms, cudaStream_t st);
+                            const AbftArgs& ab, Counters* counters, void* wsave, int num_sms, cudaStream_t st);
 
 }  // namespace tfft
 

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(K1<T, LOGN, INV, ABFT, V>::NT, K1<T, LOGN, INV
       }
       // stage-0 strikes: flip the freshly loaded element (fault.py:99-107)
       if (a.nfaults > 0 && valid) {
-        for (int f = 0; f < a.nfaults; ++f) {
+        for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
           const DevFault fl = a.faults[f];
           if (fl.signal != sig || fl.stage != 0 || (int)(fl.element % TPS) != tau) continue;
           const int k0 = (int)(fl.element / TPS);

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
       }
       if (a.nfaults > 0) {
         const int st = MODE == 0 ? 0 : a.stage;
-        for (int f = 0; f < a.nfaults; ++f) {
+        for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
           const DevFault fl = a.faults[f];
           if (fl.signal != sig || fl.stage != st) continue;
 #pragma unroll
@@ -195,11 +195,12 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
       const CT* __restrict__ lo = static_cast<const CT*>(a.lo);
       const int64_t lomask = (int64_t(1) << a.lo_bits) - 1;
       CT* d = dst + sig * a.n + p * L;
+      const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         const int q = tau + TPS * F::out_pos(k);
         if (a.nfaults > 0 && a.strike_stage == 1) {
-          for (int f = 0; f < a.nfaults; ++f) {
+          for (int f = f1; f < a.nfaults && a.faults[f].signal == sig; ++f) {
             const DevFault fl = a.faults[f];
             if (fl.signal == sig && fl.stage == 1 && fl.element == q + p * L) {
               if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);

@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
 #pragma unroll
       for (int k = 0; k < E; ++k) bad |= !finite2<T>(v[k]);
       if (a.nfaults > 0) {  // stage-0 strikes on the freshly loaded input (fault.py:99-107)
-        for (int f = 0; f < a.nfaults; ++f) {
+        for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
           const DevFault fl = a.faults[f];
           if (fl.signal != sig || fl.stage != 0) continue;
 #pragma unroll
@@ -467,13 +467,14 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       CT* d = z + ((cur.g % 3) * G + sl) * N + p * PB::CB;
       const CT step = cmul<T>(sh, sl_);
       CT w = cmul<T>(bh, bl);  // running w_N^{p (tA + TPS j)}, j ascending (<= E-1 products)
+      const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
 #pragma unroll
       for (int j = 0; j < E; ++j) {
         constexpr int RL = P::F::RLAST;
         const int k = (j % (E / RL)) * RL + j / (E / RL);  // register holding output position j
         const int q = tA + P::TPS * j;
         if (a.nfaults > 0 && a.strike_stage == 1) {  // canonical stage-1 intermediate
-          for (int f = 0; f < a.nfaults; ++f) {
+          for (int f = f1; f < a.nfaults && a.faults[f].signal == sig; ++f) {
             const DevFault fl = a.faults[f];
             if (fl.signal == sig && fl.stage == 1 && fl.element == q + (int64_t)p * N1) {
               if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
@@ -793,7 +794,7 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int k = 0; k < 16; ++k) bad |= !finite2<double>(v[k]);
       if (a.nfaults > 0) {
-        for (int f = 0; f < a.nfaults; ++f) {
+        for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
           const DevFault fl = a.faults[f];
           if (fl.signal != sig || fl.stage != 0) continue;
 #pragma unroll
@@ -819,13 +820,14 @@ __global__ void __launch_bounds__(192, 2)
       CT* d = z + ((cur.g % 3) * G + sl) * N + (int64_t)p * N1;  // p-major ring
       const CT step = cmul<double>(sh, sl_);
       CT w = cmul<double>(bh, bl);
+      const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         constexpr int RL = P::F::RLAST;
         const int k = (j % (16 / RL)) * RL + j / (16 / RL);
         const int q = tau + P::TPS * j;
         if (a.nfaults > 0 && a.strike_stage == 1) {
-          for (int f = 0; f < a.nfaults; ++f) {
+          for (int f = f1; f < a.nfaults && a.faults[f].signal == sig; ++f) {
             const DevFault fl = a.faults[f];
             if (fl.signal == sig && fl.stage == 1 && fl.element == q + (int64_t)p * N1) {
               if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);

@@ -329,7 +329,15 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
     }
     // stage-0 strikes: flip the freshly loaded element (fault.py:99-107)
     if (a.nfaults > 0 && valid) {
-      for (int f = 0; f < a.nfaults; ++f) {
+      // whole-warp signals: lane 0 searches the sorted list, the warp shares it
+      int f0;
+      if constexpr (TPS >= 32) {
+        f0 = (tid & 31) == 0 ? fault_lo(a.faults, a.nfaults, sig) : 0;
+        f0 = __shfl_sync(0xffffffffu, f0, 0);
+      } else {
+        f0 = fault_lo(a.faults, a.nfaults, sig);
+      }
+      for (int f = f0; f < a.nfaults && a.faults[f].signal == sig; ++f) {
         const DevFault fl = a.faults[f];
         if (fl.signal != sig || fl.stage != 0 || (int)(fl.element % TPS) != tau) continue;
         const int k0 = (int)(fl.element / TPS);
@@ -616,7 +624,7 @@ template <typename T, int LOGN>
 __global__ void __launch_bounds__(WinFin<T, LOGN>::NT) k5_window_finish(
     const C<T>* __restrict__ ws, const double* __restrict__ sig_part, int nws, const C<T>* __restrict__ tw,
     int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta, AbftArgs ab,
-    Counters* counters) {
+    Counters* counters, C<T>* __restrict__ wsave) {
   using WF = WinFin<T, LOGN>;
   using F = typename WF::F;
   using CT = C<T>;
@@ -647,6 +655,14 @@ __global__ void __launch_bounds__(WinFin<T, LOGN>::NT) k5_window_finish(
           vi[k] = cadd<T>(vi[k], base[tau + TPS * k]);
           vo[k] = cadd<T>(vo[k], base[N + tau + TPS * F::out_pos(k)]);
         }
+      }
+    }
+    if (wsave) {  // window sums kept for the batched correction (tfft_correct_windows)
+      CT* sv = wsave + w * 2 * (int64_t)N;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        sv[tau + TPS * k] = vi[k];
+        sv[N + tau + TPS * F::out_pos(k)] = vo[k];
       }
     }
     F::run(buf, vi, tau, tw, 1 + g);
@@ -708,7 +724,7 @@ __global__ void __launch_bounds__(WinFin<T, LOGN>::NT) k5_window_finish(
 template <typename T, int LOGN>
 static int launch_wf_t(const void* ws, const double* sig_part, int nws, const void* tw, int64_t B, int64_t W,
                        int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta, const AbftArgs& ab,
-                       Counters* counters, int num_sms, cudaStream_t st) {
+                       Counters* counters, void* wsave, int num_sms, cudaStream_t st) {
   using WF = WinFin<T, LOGN>;
   auto kern = k5_window_finish<T, LOGN>;
   static LaunchCfg cfg;
@@ -724,25 +740,25 @@ static int launch_wf_t(const void* ws, const double* sig_part, int nws, const vo
   const int64_t grid = std::min<int64_t>(want, (int64_t)num_sms * 8);
   kern<<<(unsigned)grid, WF::NT, WF::SMEM, st>>>(static_cast<const C<T>*>(ws), sig_part, nws,
                                                   static_cast<const C<T>*>(tw), B, W, G, maxseg, spt, nwin, delta,
-                                                  ab, counters);
+                                                  ab, counters, static_cast<C<T>*>(wsave));
   return (int)cudaGetLastError();
 }
 
 int launch_k5_window_finish(int prec, int logn, const void* ws, const double* sig_part, int nws, const void* tw,
                             int64_t B, int64_t W, int64_t G, int64_t maxseg, int spt, int64_t nwin, double delta,
-                            const AbftArgs& ab, Counters* counters, int num_sms, cudaStream_t st) {
+                            const AbftArgs& ab, Counters* counters, void* wsave, int num_sms, cudaStream_t st) {
 #define TFFT_WF(L)                                                                                              \
   case L:                                                                                                       \
     return prec == 0 ? launch_wf_t<float, L>(ws, sig_part, nws, tw, B, W, G, maxseg, spt, nwin, delta, ab,     \
-                                             counters, num_sms, st)                                             \
+                                             counters, wsave, num_sms, st)                                      \
                      : launch_wf_t<double, L>(ws, sig_part, nws, tw, B, W, G, maxseg, spt, nwin, delta, ab,    \
-                                              counters, num_sms, st);
+                                              counters, wsave, num_sms, st);
   switch (logn) {
     TFFT_WF(9) TFFT_WF(10) TFFT_WF(11) TFFT_WF(12)
     case 13:
       if (prec == 0)
         return launch_wf_t<float, 13>(ws, sig_part, nws, tw, B, W, G, maxseg, spt, nwin, delta, ab, counters,
-                                      num_sms, st);
+                                      wsave, num_sms, st);
       return (int)cudaErrorInvalidValue;
     default:
       return (int)cudaErrorInvalidValue;
