@@ -384,6 +384,7 @@ def abft_overheads(args, dist):
         api = None
         if name.startswith("C5"):
             api = c5_public_api(plan, x, b, T, dist, steps, args.warmup)
+        inj = injected_api(plan, x, b, T, prec, dist)
         res[name] = {"n": n, "batch_per_gpu": b, "T": T, "bs": plan.bs, "plain_ms": round(tp * 1e3, 4),
                      "fused_ms": round(tfz * 1e3, 4), "overhead_pct": round(100 * (tfz / tp - 1), 2),
                      "plain_gbs": round(gbs, 1),
@@ -391,6 +392,7 @@ def abft_overheads(args, dist):
                              if n <= 4096 else ("K7" if prec == "double" else "K4") + " transform + one-sweep checksums"}
         if api is not None:
             res[name]["public_api"] = api
+        res[name]["injected"] = inj
         del x, y, sums
         torch.cuda.empty_cache()
     return res
@@ -537,6 +539,55 @@ def c4_config(args, dist, peak):
             del x, y, sums
             torch.cuda.empty_cache()
     return out
+
+
+def injected_api(plan, x, b, T, prec, dist, reps=3):
+    """ABFT under injection through the public API (run_protected on the
+    device batch): one mantissa-top-bit fault in EVERY verification window
+    (stage 0, random element), min wall time of `reps` calls, against the
+    same call without faults. Detected faults are corrected online (batched
+    correction of single-trigger windows, the serial replay for the rest)."""
+    import torch
+
+    import paper_2412_05824_b200 as tf
+
+    n = x.shape[1]
+    batch = tf.SignalBatch(x)
+    ntx = -(-b // plan.bs)
+    nwin = -(-ntx // T)
+    rng = np.random.default_rng(0xC3)
+    bit = 22 if prec == "single" else 51
+    specs = []
+    for w in range(nwin):
+        tx = min(w * T + int(rng.integers(T)), ntx - 1)
+        sig = tx * plan.bs + int(rng.integers(min(plan.bs, b - tx * plan.bs)))
+        specs.append(dict(transaction=tx, signal=sig, element=int(rng.integers(n)), stage=0, part="re", bit=bit))
+
+    def injector():
+        i = tf.FaultInjector(seu=False)
+        for sp in specs:
+            i.arm(tf.FaultSpec(**sp), plan=plan, batch=batch)
+        return i
+
+    tf.run_protected(plan, batch, group_size=T, injector=injector())  # warm (correction plan, workspaces)
+    tc, ti, stats = [], [], None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tf.run_protected(plan, batch, group_size=T)
+        torch.cuda.synchronize()
+        tc.append(time.perf_counter() - t0)
+        j, stats = injector(), tf.RunStats()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tf.run_protected(plan, batch, group_size=T, injector=j, stats=stats)
+        torch.cuda.synchronize()
+        ti.append(time.perf_counter() - t0)
+    c, i = dist.max(min(tc)), dist.max(min(ti))
+    return {"injections": len(specs), "bit": bit, "events": len(stats.events), "corrections": stats.corrections,
+            "recomputations": stats.recomputations, "api_clean_ms": round(c * 1e3, 3),
+            "api_injected_ms": round(i * 1e3, 3), "injection_overhead_pct": round(100 * (i / c - 1), 1),
+            "call": "run_protected(SignalBatch(device tensor), group_size=T[, injector])"}
 
 
 def c5_public_api(plan, x, b, T, dist, steps, warmup):
