@@ -503,7 +503,7 @@ def c4_config(args, dist, peak):
                 batch = tf.SignalBatch(x)
                 rng = np.random.default_rng(0xC4)
                 # mantissa-top bit: the per-signal test fires and the fault is corrected online
-                bit = 22 if prec == "single" else 51
+                bit = 24 if prec == "single" else 51  # FP32: exponent bit 1 (x4 or /4), FP64: mantissa top bit
                 specs = []
                 for w in range(nwin):
                     tx = w * T + int(rng.integers(0, T))
@@ -512,7 +512,8 @@ def c4_config(args, dist, peak):
                 # warm-up: left row, workspaces and the FP64 correction plan
                 # (built on first use) outside the timed calls
                 warm = tf.FaultInjector(seu=False)
-                warm.arm(specs[0], plan=plan, batch=batch)
+                for sp in specs:
+                    warm.arm(sp, plan=plan, batch=batch)
                 tf.run_protected(plan, batch, group_size=T, injector=warm)
                 specs = [tf.FaultSpec(**{k: getattr(sp, k) for k in ("transaction", "signal", "element", "stage",
                                                                       "part", "bit")}) for sp in specs]
@@ -556,7 +557,7 @@ def injected_api(plan, x, b, T, prec, dist, reps=3):
     ntx = -(-b // plan.bs)
     nwin = -(-ntx // T)
     rng = np.random.default_rng(0xC3)
-    bit = 22 if prec == "single" else 51
+    bit = 24 if prec == "single" else 51  # FP32: exponent bit 1 (x4 or /4), FP64: mantissa top bit
     specs = []
     for w in range(nwin):
         tx = min(w * T + int(rng.integers(T)), ntx - 1)

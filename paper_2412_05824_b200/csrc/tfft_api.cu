@@ -849,14 +849,32 @@ int tfft_correction_column(tfft_plan* p, const void* snap_in, const void* snap_o
   return TFFT_OK;
 }
 
+static int correct_windows_chunk(tfft_plan* p, const void* x, void* y, int64_t signal_offset, int64_t count,
+                                 const int64_t* desc_host, const double* par_host, int enc, double delta,
+                                 double* out_host, cudaStream_t st);
+
 int tfft_correct_windows(tfft_plan* p, const void* x, void* y, int64_t signal_offset, int64_t count,
                          const int64_t* desc_host, const double* par_host, int enc, double delta, double* out_host,
                          void* stream) {
   if (!p || !x || !y || count < 0 || (count && (!desc_host || !par_host || !out_host)))
     return fail(TFFT_EINVAL, "invalid correct_windows arguments");
   if (count == 0) return TFFT_OK;
+  // items in chunks of <= 256 MB of working vectors (7 per item)
+  int64_t per = ((int64_t)256 << 20) / (p->n * 16);
+  if (per < 1) per = 1;
+  for (int64_t i0 = 0; i0 < count; i0 += per) {
+    const int64_t c = count - i0 < per ? count - i0 : per;
+    int rc = correct_windows_chunk(p, x, y, signal_offset, c, desc_host + 6 * i0, par_host + 4 * i0, enc, delta,
+                                   out_host + 4 * i0, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return TFFT_OK;
+}
+
+static int correct_windows_chunk(tfft_plan* p, const void* x, void* y, int64_t signal_offset, int64_t count,
+                                 const int64_t* desc_host, const double* par_host, int enc, double delta,
+                                 double* out_host, cudaStream_t st) {
   if (enc != ENC_WANG && enc != ENC_ONES) return fail(TFFT_EUNSUPPORTED, "batched correction: wang / ones only");
-  cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = p->n;
   const size_t cb = cbytes(p->prec);
   const size_t vec = (size_t)count * n * cb;

@@ -37,6 +37,10 @@
 #include "tfft_internal.h"
 #include "tfft_k4.h"
 
+#ifndef TFFT_K7_EXP
+#define TFFT_K7_EXP 0
+#endif
+
 namespace tfft {
 
 // cuTensorMapEncodeTiled through cudaGetDriverEntryPoint (resolved once)
@@ -816,7 +820,9 @@ __global__ void __launch_bounds__(192, 2)
         fft_sync<NT>();
         staged = false;
       }
+#if !(TFFT_K7_EXP & 1)  // experiment: FFT arithmetic compiled out (data path only)
       P::F::run(slots + g * P::SLOTQ, v, tau, tws1, 2 + g);
+#endif
       CT* d = z + ((cur.g % 3) * G + sl) * N + (int64_t)p * N1;  // p-major ring
       const CT step = cmul<double>(sh, sl_);
       CT w = cmul<double>(bh, bl);
@@ -864,7 +870,9 @@ __global__ void __launch_bounds__(192, 2)
         fft_sync<NT>();
         staged = false;
       }
+#if !(TFFT_K7_EXP & 1)
       P::F::run(slots + g * P::SLOTQ, v, tau, tws2, 2 + g);
+#endif
       // outputs -> swizzled [k][column] staging (aliasing the slots: once every
       // column's FFT is done) -> 2-D TMA stores into y
       if (!K::ALIAS && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
