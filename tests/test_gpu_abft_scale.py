@@ -36,16 +36,26 @@ def _left_row(n, dtype):
     return np.fft.fft(e).astype(np.complex128)  # sum_j e_j exp(-2 pi i j k / n)
 
 
-@pytest.mark.parametrize("mode", ["default", "fused", "sweep"])
-@pytest.mark.parametrize("precision,n,b,T", CASES, ids=lambda v: str(v))
-def test_protected_sums_match_fp64_recomputation(precision, n, b, T, mode, monkeypatch):
-    import torch
-
-    if mode != "default":
+def _route(mode, n, monkeypatch):
+    """default; the fused K5 or the one-sweep route for single-pass sizes; the
+    opt-in fused K4 C tiles (TFFT_K4_ABFT=1) for two-pass sizes"""
+    if mode == "k4fused":
+        if n <= 4096:
+            pytest.skip("two-pass sizes only")
+        monkeypatch.setenv("TFFT_K4_ABFT", "1")
+    elif mode != "default":
         if n > 4096:
             pytest.skip("no fused kernel at this size")
         # both protected routes for the fused sizes (tfft_api.cu abft_use_sweep)
         monkeypatch.setenv("TFFT_ABFT_SWEEP", "1" if mode == "sweep" else "0")
+
+
+@pytest.mark.parametrize("mode", ["default", "fused", "sweep", "k4fused"])
+@pytest.mark.parametrize("precision,n,b,T", CASES, ids=lambda v: str(v))
+def test_protected_sums_match_fp64_recomputation(precision, n, b, T, mode, monkeypatch):
+    import torch
+
+    _route(mode, n, monkeypatch)
     tf = _tf()
     from paper_2412_05824_b200 import abft as A, fft_core
     x = gaussian(n, b, precision, seed=n + b)
@@ -94,13 +104,10 @@ def test_protected_sums_match_fp64_recomputation(precision, n, b, T, mode, monke
     assert ctr.read()["triggered"] == 0  # nothing triggered
 
 
-@pytest.mark.parametrize("mode", ["default", "fused", "sweep"])
+@pytest.mark.parametrize("mode", ["default", "fused", "sweep", "k4fused"])
 @pytest.mark.parametrize("precision,n,b,T", CASES, ids=lambda v: str(v))
 def test_single_fault_detected_and_corrected_at_scale(precision, n, b, T, mode, monkeypatch):
-    if mode != "default":
-        if n > 4096:
-            pytest.skip("no fused kernel at this size")
-        monkeypatch.setenv("TFFT_ABFT_SWEEP", "1" if mode == "sweep" else "0")
+    _route(mode, n, monkeypatch)
     tf = _tf()
     x = gaussian(n, b, precision, seed=3 * n + b)
     plan = tf.build_plan(tf.select_params(n, b, precision), precision)
