@@ -148,15 +148,22 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
       // DIT Stockham stage: leg t of column j = q + S p' times w_{S L}^{q t}
       // (= w_N^{q t N / (S L)}, two-level table), then the L-point DFT
       if (a.s > 1) {
+        // w_N^{m}, m = q t N / (S L), t = tau + TPS k: the base (t = tau) and
+        // the step (TPS) from the two-level table, then E - 1 products (as
+        // K4's pass A) instead of two table loads per leg
         const CT* __restrict__ hi = static_cast<const CT*>(a.hi);
         const CT* __restrict__ lo = static_cast<const CT*>(a.lo);
         const int64_t lomask = (int64_t(1) << a.lo_bits) - 1;
         const int64_t q = (c0 + g) & (a.s - 1);
         const int64_t scale = a.n / (a.s * L);
+        const int64_t mb = (q * (int64_t)tau * scale) & (a.n - 1);
+        const int64_t ms = (q * (int64_t)TPS * scale) & (a.n - 1);
+        CT w = cmul<T>(__ldg(hi + (mb >> a.lo_bits)), __ldg(lo + (mb & lomask)));
+        const CT step = cmul<T>(__ldg(hi + (ms >> a.lo_bits)), __ldg(lo + (ms & lomask)));
 #pragma unroll
         for (int k = 0; k < E; ++k) {
-          const int64_t m = q * (int64_t)(tau + TPS * k) * scale;
-          v[k] = cmul<T>(v[k], cmul<T>(__ldg(hi + (m >> a.lo_bits)), __ldg(lo + (m & lomask))));
+          v[k] = cmul<T>(v[k], w);
+          if (k + 1 < E) w = cmul<T>(w, step);
         }
       }
     }
