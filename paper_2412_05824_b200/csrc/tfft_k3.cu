@@ -73,8 +73,12 @@ struct ColArgs {
   int last;         // last stage (inverse: x 1/N)
 };
 
+// stage passes: two CTAs per SM (TFFT_COL2_MINB=2) spill and measured 15-20% slower
+#ifndef TFFT_COL2_MINB
+#define TFFT_COL2_MINB 1
+#endif
 template <typename T, int LOGL, bool INV, int MODE>
-__global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) col_kernel(ColArgs a) {
+__global__ void __launch_bounds__(ColCfg<T, LOGL>::NT, MODE == 2 ? TFFT_COL2_MINB : 1) col_kernel(ColArgs a) {
   using K = ColCfg<T, LOGL>;
   using F = Fft<T, K::L, K::EMAX, INV>;
   using CT = C<T>;
