@@ -640,6 +640,36 @@ int tfft_protected(tfft_plan* p, const void* x, void* y, int64_t batch, int64_t 
     TFFT_TRY(launch_k1(p->prec, p->logn, false, true, a, p->num_sms, st), "k1 abft launch");
   } else {
     const size_t cb = cbytes(p->prec);
+    // three-stage plans, opt-in (TFFT_STAGE_ABFT=1): the checksums and window
+    // sums fused into the first and last stage passes, FFT(s_in) carried along
+    // as pseudo-signals. Correct (the C4 decision tests pass with it on) but
+    // slower than the plain passes + one sweep: the per-item accumulators and
+    // row slices spill the pass kernels (64-255 registers, 0.4-1.6 KB spills)
+    // and at W = 1 (bs = 1, T = 1: 2^24, 2^25) the row is re-read per window.
+    if (p->mode == 2 && p->stg && slow.empty() && !abft_force_sweep() && enc != ENC_JOU &&
+        std::getenv("TFFT_STAGE_ABFT") != nullptr) {
+      int64_t parts = 0, gper = 0;
+      int e = stage_protected_parts(p->stg, &parts, &gper);
+      if (!e) e = p->scratch_b.ensure((size_t)batch * p->n * cb);
+      if (!e) e = p->scratch_a.ensure((size_t)2 * nwin * p->n * cb);
+      if (!e) e = p->sigpart.ensure((size_t)batch * parts * 5 * sizeof(double));
+      if (!e) e = p->part.ensure((size_t)nwin * gper * 2 * sizeof(double));
+      if (e) return cuda_fail(e, "stage abft workspace");
+      char* pa = (char*)p->scratch_a.p;
+      char* pb = pa + (size_t)nwin * p->n * cb;
+      int rk = stage_protected(p->stg, x, y, p->scratch_b.p, batch, signal_offset, (const DevFault*)p->faults.p,
+                               (int)dev.size(), (Counters*)counters, W, enc, p->rows[enc].p, pa, pb,
+                               (double*)p->sigpart.p, (double*)p->part.p, sums->win_div, st);
+      if (rk != (int)cudaErrorNotSupported) {
+        if (rk) return cuda_fail(rk, "stage abft launch");
+        g_launches.fetch_add(stage_count(p->stg) + 2, std::memory_order_relaxed);
+        p->sums_kind = 0;
+        TFFT_TRY(launch_signal_epilogue((const double*)p->sigpart.p, parts, p->n, batch, delta, ab,
+                                        (Counters*)counters, st),
+                 "abft signal epilogue");
+        return TFFT_OK;
+      }
+    }
     // two-pass sizes on K4, opt-in (TFFT_K4_ABFT=1): the checksums fused into
     // the transform's launch (C tiles over L2-resident x and y), then the
     // window FFT, the group divergence and the per-signal decisions. Correct

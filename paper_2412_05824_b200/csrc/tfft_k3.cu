@@ -360,6 +360,302 @@ int ilog2i(int64_t v) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// Fused two-sided ABFT over the stage passes (abft.py:648-665, :592-624).
+// The first and the last stage walk items (window w, column block): the CB
+// columns of every signal of the window in turn, then one pseudo-signal.
+//  first stage (PH 0): c_in = row . x and ||x||^2 partials from the loaded
+//    legs (the row slice is read once per item), s_in += w_j x_j in
+//    registers; after the window's signals the pseudo-signal s_in gets the
+//    same stage pass, written to its own buffer -- so the later stages carry
+//    FFT(s_in) along at 1/W extra work instead of a separate window FFT;
+//  last stage (PH 2): c_out partials and s_out += w_j y_j from the outputs;
+//    the pseudo-signal's output IS FFT(s_in), compared in place with s_out
+//    (group-divergence partials). x and y are read / written exactly once.
+struct StageAbft {
+  int64_t win;         // W = T * bs signals per window
+  int64_t nwin;
+  int64_t weight0;     // global index of row 0
+  const void* row;     // left checksum row
+  int enc;             // ENC_WANG / ENC_ONES
+  void* pseudo_dst;    // [nwin][N] (PH 0 output of the pseudo-signals)
+  const void* pseudo_src;  // [nwin][N] (PH 2 input)
+  double* sig_part;    // [B][P][5]: PH 0 fills 0..2, PH 2 fills 3..4 (zeroed)
+  int64_t parts;       // P
+  double* gpart;       // [nwin][ncb * NW][2] (PH 2)
+};
+
+template <typename T, int LOGL, int PH>
+__global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) stage_abft_kernel(ColArgs a, StageAbft b) {
+  using K = ColCfg<T, LOGL>;
+  using F = Fft<T, K::L, K::EMAX, false>;
+  using CT = C<T>;
+  constexpr int L = K::L, E = K::E, TPS = K::TPS, CB = K::CB, NT = K::NT, NW = NT / 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  CT* tile = reinterpret_cast<CT*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const int g = tid / TPS;
+  const int tau = tid % TPS;
+  CT* slot = tile + K::base(g);
+  const CT* __restrict__ src = static_cast<const CT*>(a.src);
+  CT* __restrict__ dst = static_cast<CT*>(a.dst);
+  const CT* __restrict__ tw = static_cast<const CT*>(a.tw);
+  const int64_t ncb = a.ncols / CB;
+  const int64_t nitems = b.nwin * ncb;
+  bool bad = false;
+  CT ld[E];
+  // one sub-tile: signal sig (pseudo when sig >= batch) of column block c0
+  auto issue = [&](const CT* base) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int e = i * NT + tid;
+      ld[i] = __ldcs(base + (int64_t)(e / CB) * a.pitch + e % CB);
+    }
+  };
+  auto land = [&]() {
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int e = i * NT + tid;
+      tile[K::base(e % CB) + F::phys(e / CB)] = ld[i];
+    }
+    __syncthreads();
+  };
+  auto warp_sum = [&](T v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = radd(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+  };
+
+  // the first load of item `it` (its window's first signal)
+  auto item_base = [&](int64_t it) {
+    const int64_t w = it / ncb, cb = it % ncb;
+    return src + (w * b.win) * a.n + cb * CB;
+  };
+  if ((int64_t)blockIdx.x < nitems) issue(item_base(blockIdx.x));
+#pragma unroll 1
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int64_t w = it / ncb, cb = it % ncb;
+    const int64_t c0 = cb * CB;
+    const int64_t w0 = w * b.win, w1 = min(w0 + b.win, a.batch);
+    const int64_t col = c0 + g;
+    const int64_t itn = it + gridDim.x;  // the next item: its first load is issued during this one's last sub-tile
+    CT acc[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) acc[k] = mk<T>(0, 0);
+    CT rw[E];
+    if constexpr (PH == 0) {
+      const CT* __restrict__ row = static_cast<const CT*>(b.row);
+#pragma unroll
+      for (int k = 0; k < E; ++k) rw[k] = __ldg(row + col + (int64_t)(tau + TPS * k) * a.pitch);
+    }
+    // twiddle base / step of this column (last stage, S > 1): w_N^{q t N / (S L)}
+    CT tw0 = mk<T>(1, 0), tstep = mk<T>(1, 0);
+    if constexpr (PH == 2) {
+      const CT* __restrict__ hi = static_cast<const CT*>(a.hi);
+      const CT* __restrict__ lo = static_cast<const CT*>(a.lo);
+      const int64_t lomask = (int64_t(1) << a.lo_bits) - 1;
+      const int64_t q = col & (a.s - 1);
+      const int64_t scale = a.n / (a.s * L);
+      const int64_t mb = (q * (int64_t)tau * scale) & (a.n - 1);
+      const int64_t ms = (q * (int64_t)TPS * scale) & (a.n - 1);
+      tw0 = cmul<T>(__ldg(hi + (mb >> a.lo_bits)), __ldg(lo + (mb & lomask)));
+      tstep = cmul<T>(__ldg(hi + (ms >> a.lo_bits)), __ldg(lo + (ms & lomask)));
+    }
+#pragma unroll 1
+    for (int64_t j = w0; j <= w1; ++j) {  // j == w1: the window's pseudo-signal
+      const bool pseudo = j == w1;
+      if (PH == 0 && pseudo) {
+        __syncthreads();  // the slots' last readers are done
+      } else {
+        land();
+      }
+      // next sub-tile's loads in flight during this one's passes (across items)
+      if (j + 1 < w1) issue(src + (j + 1) * a.n + c0);
+      else if (PH == 2 && j + 1 == w1) issue(static_cast<const CT*>(b.pseudo_src) + w * a.n + c0);
+      else if (((PH == 0 && j + 1 == w1) || (PH == 2 && pseudo)) && itn < nitems) issue(item_base(itn));
+      CT v[E];
+      if (PH == 0 && pseudo) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = acc[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = slot[F::phys(tau + TPS * k)];
+      }
+      const T wj = (T)(b.weight0 + j + 1);
+      if constexpr (PH == 0) {
+        if (!pseudo) {
+          // c_in, ||x||^2 and s_in from the clean legs, then the strikes
+          T r5[3] = {0, 0, 0};
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            bad |= !finite2<T>(v[k]);
+            r5[0] = rfma(rw[k].x, v[k].x, rfma(-rw[k].y, v[k].y, r5[0]));
+            r5[1] = rfma(rw[k].x, v[k].y, rfma(rw[k].y, v[k].x, r5[1]));
+            r5[2] = rfma(v[k].x, v[k].x, rfma(v[k].y, v[k].y, r5[2]));
+            acc[k] = mk<T>(rfma(wj, v[k].x, acc[k].x), rfma(wj, v[k].y, acc[k].y));
+          }
+#pragma unroll
+          for (int q = 0; q < 3; ++q) r5[q] = warp_sum(r5[q]);
+          if (lane == 0) {
+            double* dp = b.sig_part + (j * b.parts + cb * NW + wp) * 5;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) dp[q] = (double)r5[q];
+          }
+        }
+      }
+      if (!pseudo && a.nfaults > 0) {  // this stage's strikes on the canonical intermediate
+        for (int f = fault_lo(a.faults, a.nfaults, j); f < a.nfaults && a.faults[f].signal == j; ++f) {
+          const DevFault fl = a.faults[f];
+          if (fl.stage != a.stage) continue;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (col + (int64_t)(tau + TPS * k) * a.pitch == fl.element) {
+              if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
+              else v[k].y = flip_bits(v[k].y, fl.bit);
+            }
+        }
+      }
+      if constexpr (PH == 2) {
+        CT wv = tw0;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          v[k] = cmul<T>(v[k], wv);
+          if (k + 1 < E) wv = cmul<T>(wv, tstep);
+        }
+      }
+      F::run(slot, v, tau, tw);
+      if constexpr (PH == 0) {
+        // stage 0 (S = 1): column j's outputs are contiguous at j L + c
+        CT* d = pseudo ? static_cast<CT*>(b.pseudo_dst) + w * a.n + col * L : dst + j * a.n + col * L;
+#pragma unroll
+        for (int k = 0; k < E; ++k) __stcs(d + tau + TPS * F::out_pos(k), v[k]);
+        __syncthreads();
+      } else {
+        if (!pseudo) {
+          // outputs at e = q + S c: c_out (wang: omega_3^(e mod 3)) and s_out
+          T r2[2] = {0, 0};
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const int64_t e = col + a.s * (int64_t)(tau + TPS * F::out_pos(k));
+            CT ev = mk<T>(1, 0);
+            if (b.enc == ENC_WANG) {
+              const int m = (int)(e % 3);
+              const T h = (T)0.86602540378443864676372317075294;
+              ev = m == 0 ? mk<T>(1, 0) : (m == 1 ? mk<T>((T)-0.5, -h) : mk<T>((T)-0.5, h));
+            }
+            r2[0] = rfma(ev.x, v[k].x, rfma(-ev.y, v[k].y, r2[0]));
+            r2[1] = rfma(ev.x, v[k].y, rfma(ev.y, v[k].x, r2[1]));
+            acc[k] = mk<T>(rfma(wj, v[k].x, acc[k].x), rfma(wj, v[k].y, acc[k].y));
+          }
+          r2[0] = warp_sum(r2[0]);
+          r2[1] = warp_sum(r2[1]);
+          if (lane == 0) {
+            double* dp = b.sig_part + (j * b.parts + cb * NW + wp) * 5;
+            dp[3] = (double)r2[0];
+            dp[4] = (double)r2[1];
+          }
+          // y: transposed through the slots, CB contiguous per output row
+          __syncthreads();
+#pragma unroll
+          for (int k = 0; k < E; ++k) slot[F::phys(tau + TPS * F::out_pos(k))] = v[k];
+          __syncthreads();
+          CT* d = dst + j * a.n + c0;
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const int e = i * NT + tid;
+            const int r = e / CB, c = e % CB;
+            __stcs(d + (int64_t)r * a.s + c, tile[K::base(c) + F::phys(r)]);
+          }
+          __syncthreads();
+        } else {
+          // the pseudo-signal's output is ref = FFT(s_in): group partials
+          double a2 = 0, b2 = 0;
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const double dr = (double)v[k].x - (double)acc[k].x, di = (double)v[k].y - (double)acc[k].y;
+            a2 += dr * dr + di * di;
+            b2 += (double)v[k].x * (double)v[k].x + (double)v[k].y * (double)v[k].y;
+          }
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) {
+            a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+            b2 += __shfl_xor_sync(0xffffffffu, b2, off);
+          }
+          if (lane == 0) {
+            b.gpart[((w * ncb + cb) * NW + wp) * 2] = a2;
+            b.gpart[((w * ncb + cb) * NW + wp) * 2 + 1] = b2;
+          }
+          __syncthreads();
+        }
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
+}
+
+// group_div[w] = sqrt(sum a) / max(sqrt(sum b), 1e-30) over the window's partials, in order
+__global__ void stage_group_fin_kernel(const double* gpart, int64_t per, int64_t nwin, double* out) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= nwin) return;
+  double a2 = 0, b2 = 0;
+  for (int64_t i = 0; i < per; ++i) {
+    a2 += gpart[(w * per + i) * 2];
+    b2 += gpart[(w * per + i) * 2 + 1];
+  }
+  out[w] = sqrt(a2) / fmax(sqrt(b2), 1e-30);
+}
+
+template <typename T, int LOGL, int PH>
+static int launch_stage_abft_t(const ColArgs& a, const StageAbft& b, int num_sms, cudaStream_t st) {
+  using K = ColCfg<T, LOGL>;
+  auto kern = stage_abft_kernel<T, LOGL, PH>;
+  static LaunchCfg cfg;
+  const int dev = current_device();
+  if (!cfg.done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    int ps = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, K::NT, K::SMEM);
+    if (e != cudaSuccess) return (int)e;
+    cfg.per_sm[dev] = ps < 1 ? 1 : ps;
+    cfg.done[dev] = true;
+  }
+  const int64_t nitems = b.nwin * (a.ncols / K::CB);
+  int64_t grid = (int64_t)num_sms * cfg.per_sm[dev];
+  if (grid > nitems) grid = nitems;
+  if (grid < 1) return 0;
+  kern<<<(unsigned)grid, K::NT, K::SMEM, st>>>(a, b);
+  return (int)cudaGetLastError();
+}
+
+template <typename T, int PH>
+static int dispatch_stage_abft(int logl, const ColArgs& a, const StageAbft& b, int num_sms, cudaStream_t st) {
+  switch (logl) {
+#define TFFT_SA(L) \
+  case L: return launch_stage_abft_t<T, L, PH>(a, b, num_sms, st);
+    TFFT_SA(6) TFFT_SA(7) TFFT_SA(8) TFFT_SA(9) TFFT_SA(10) TFFT_SA(11)
+#undef TFFT_SA
+    default:
+      return (int)cudaErrorInvalidValue;
+  }
+}
+
+template <int PH>
+static int stage_abft(int prec, int logl, const ColArgs& a, const StageAbft& b, int num_sms, cudaStream_t st) {
+  return prec == 0 ? dispatch_stage_abft<float, PH>(logl, a, b, num_sms, st)
+                   : dispatch_stage_abft<double, PH>(logl, a, b, num_sms, st);
+}
+
+// warps per stage-pass tile (NT / 32) and column blocks of a span
+static void stage_tile_shape(int prec, int64_t L, int64_t n, int64_t* ncb, int* nw) {
+  const int bpc = prec == 0 ? 8 : 16;
+  int64_t cb0 = 65536 / (L * bpc);
+  const int64_t cb = cb0 < 2 ? 2 : (cb0 > 32 ? 32 : cb0);
+  const int64_t tps = L / (16 < L ? 16 : L);
+  *ncb = (n / L) / cb;
+  *nw = (int)((cb * tps) / 32);
+}
+
+// ---------------------------------------------------------------------------
 // stage passes
 
 struct StagePlan {
@@ -415,6 +711,90 @@ void stage_destroy(StagePlan* p) {
 }
 
 int stage_count(const StagePlan* p) { return p ? p->nst : 0; }
+
+int stage_protected_parts(const StagePlan* p, int64_t* parts, int64_t* gper) {
+  // [B][P][5] per-signal partials with P = the larger of the first and last
+  // stage's (column blocks x warps); per-window group partials of the last
+  int64_t ncb0, ncb2;
+  int nw0, nw2;
+  stage_tile_shape(p->prec, p->spans[0], p->n, &ncb0, &nw0);
+  stage_tile_shape(p->prec, p->spans[p->nst - 1], p->n, &ncb2, &nw2);
+  if (nw0 < 1 || nw2 < 1) return (int)cudaErrorNotSupported;
+  *parts = ncb0 * nw0 > ncb2 * nw2 ? ncb0 * nw0 : ncb2 * nw2;
+  *gper = ncb2 * nw2;
+  return 0;
+}
+
+int stage_protected(StagePlan* p, const void* x, void* y, void* tmp, int64_t batch, int64_t weight0,
+                    const DevFault* faults, int nfaults, Counters* counters, int64_t win, int enc, const void* row,
+                    void* pa, void* pb, double* sig_part, double* gpart, double* win_div, cudaStream_t st) {
+  if (p->nst < 2 || (enc != ENC_WANG && enc != ENC_ONES)) return (int)cudaErrorNotSupported;
+  int64_t parts = 0, gper = 0;
+  int rc = stage_protected_parts(p, &parts, &gper);
+  if (rc) return rc;
+  const int64_t nwin = (batch + win - 1) / win;
+  cudaError_t e = cudaMemsetAsync(sig_part, 0, (size_t)batch * parts * 5 * sizeof(double), st);
+  if (e != cudaSuccess) return (int)e;
+  StageAbft b{};
+  b.win = win;
+  b.nwin = nwin;
+  b.weight0 = weight0;
+  b.row = row;
+  b.enc = enc;
+  b.sig_part = sig_part;
+  b.parts = parts;
+  b.gpart = gpart;
+  const void* src = x;
+  void* psrc = nullptr;
+  int64_t S = 1;
+  for (int k = 0; k < p->nst; ++k) {
+    void* dst = ((p->nst - 1 - k) % 2 == 0) ? y : tmp;
+    void* pdst = (k % 2 == 0) ? pa : pb;
+    const int64_t L = p->spans[k];
+    ColArgs a{};
+    a.src = src;
+    a.dst = dst;
+    a.batch = batch;
+    a.n = p->n;
+    a.pitch = p->n / L;
+    a.ncols = p->n / L;
+    a.tw = p->tw[k][0];
+    a.hi = p->hi[0];
+    a.lo = p->lo[0];
+    a.lo_bits = p->lo_bits;
+    a.faults = faults;
+    a.nfaults = nfaults;
+    a.strike_stage = -1;
+    a.counters = counters;
+    a.s = S;
+    a.stage = k;
+    a.last = 0;
+    if (k == 0) {
+      b.pseudo_dst = pdst;
+      rc = stage_abft<0>(p->prec, ilog2i(L), a, b, p->num_sms, st);
+    } else if (k == p->nst - 1) {
+      b.pseudo_src = psrc;
+      rc = stage_abft<2>(p->prec, ilog2i(L), a, b, p->num_sms, st);
+    } else {
+      rc = col(p->prec, false, 2, ilog2i(L), a, p->num_sms, st);  // the real signals
+      if (!rc) {
+        ColArgs q = a;  // the pseudo-signals (no strikes, no counters)
+        q.src = psrc;
+        q.dst = pdst;
+        q.batch = nwin;
+        q.nfaults = 0;
+        q.counters = nullptr;
+        rc = col(p->prec, false, 2, ilog2i(L), q, p->num_sms, st);
+      }
+    }
+    if (rc) return rc;
+    src = dst;
+    psrc = pdst;
+    S *= L;
+  }
+  stage_group_fin_kernel<<<(unsigned)((nwin + 127) / 128), 128, 0, st>>>(gpart, gper, nwin, win_div);
+  return (int)cudaGetLastError();
+}
 
 int stage_execute(StagePlan* p, const void* x, void* y, void* tmp, int64_t batch, int inverse, const DevFault* faults,
                   int nfaults, Counters* counters, cudaStream_t st) {

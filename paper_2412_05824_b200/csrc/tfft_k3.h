@@ -43,5 +43,13 @@ void stage_destroy(StagePlan* p);
 int stage_execute(StagePlan* p, const void* x, void* y, void* tmp, int64_t batch, int inverse, const DevFault* faults,
                   int nfaults, Counters* counters, cudaStream_t st);
 int stage_count(const StagePlan* p);
+// Fused two-sided ABFT over the stage passes (forward): checksums and window
+// sums in the first / last stage, FFT(s_in) carried as pseudo-signals through
+// pa / pb ([nwin][n] each). Outputs per-signal partials [B][*parts][5] (for
+// launch_signal_epilogue) and win_div. cudaErrorNotSupported when not applicable.
+int stage_protected_parts(const StagePlan* p, int64_t* parts, int64_t* gper);
+int stage_protected(StagePlan* p, const void* x, void* y, void* tmp, int64_t batch, int64_t weight0,
+                    const DevFault* faults, int nfaults, Counters* counters, int64_t win, int enc, const void* row,
+                    void* pa, void* pb, double* sig_part, double* gpart, double* win_div, cudaStream_t st);
 
 }  // namespace tfft

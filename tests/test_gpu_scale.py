@@ -189,10 +189,16 @@ def _want(rec):
             [tuple(q[:3]) for q in rec["reports"]])
 
 
+@pytest.mark.parametrize("route", ["default", "stage_abft"])
 @pytest.mark.parametrize("camp", scale()["campaigns"], ids=lambda c: c["name"])
-def test_scale_campaign_decisions(camp):
+def test_scale_campaign_decisions(camp, route, monkeypatch):
     """C3 / C4 / C5-scale single-fault trials: events, corrections,
-    recomputations and report flags equal to the reference's."""
+    recomputations and report flags equal to the reference's (three-stage
+    plans also through the opt-in fused stage-pass ABFT)."""
+    if route == "stage_abft":
+        if len(camp["spans"]) < 3:
+            pytest.skip("three-stage plans only")
+        monkeypatch.setenv("TFFT_STAGE_ABFT", "1")
     tf = _tf()
     from paper_2412_05824_b200 import fault as F
     params = tf.PlanParams(tuple(camp["spans"]), tuple(camp["radices"]), camp["bs"])
