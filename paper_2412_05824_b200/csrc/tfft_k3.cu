@@ -894,7 +894,11 @@ int k3_launches(const K3Plan* p) { return p && p->k4 ? 1 : 2; }
 // K4 group size: ~16 MB of intermediate per group, so the 3-slot ring is ~48 MB
 static int64_t k4_group(const K3Plan* p, int64_t batch) {
   const int64_t cb = p->prec == 0 ? 8 : 16;
-  int64_t g = (int64_t(16) << 20) / (p->n * cb);
+  // ~16 MB of intermediate per group (3-slot ring ~48 MB) up to 2^16; 32 MB
+  // from 2^17 (measured sweep 4..48 MB: 2^18..2^20 FP64 2-4% and FP32 3-7%
+  // faster, 2^14..2^16 slower with the larger ring)
+  const int64_t mb = p->n >= (int64_t(1) << 17) ? 32 : 16;
+  int64_t g = (mb << 20) / (p->n * cb);
   if (g < 1) g = 1;
   if (g > batch) g = batch;
   return g;
