@@ -431,15 +431,49 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
         // at C3 FP32).
         constexpr int W0 = TPS < 32 ? TPS : 32;
         constexpr int NWS = TPS >= 32 ? TPS / 32 : 1;
-        T r5[5] = {(T)red5[0], (T)red5[1], (T)red5[2], (T)red5[3], (T)red5[4]};
+        if constexpr (W0 == 32) {
+          // transposed (recursive-halving) reduction of the 5 values padded to
+          // 8: 4 + 2 + 1 + 1 + 1 = 9 shuffles instead of 25; lane 4 i ends
+          // with value i (fixed order, deterministic)
+          const int ln = tid & 31;
+          T r8[8] = {(T)red5[0], (T)red5[1], (T)red5[2], (T)red5[3], (T)red5[4], (T)0, (T)0, (T)0};
+          const bool h4 = ln & 16, h3 = ln & 8, h2 = ln & 4;
+          T s4[4];
 #pragma unroll
-        for (int off = W0 / 2; off >= 1; off >>= 1)
+          for (int i = 0; i < 4; ++i) {
+            const T send = h4 ? r8[i] : r8[i + 4];
+            const T keep = h4 ? r8[i + 4] : r8[i];
+            s4[i] = radd(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+          }
+          T s2[2];
 #pragma unroll
-          for (int kk = 0; kk < 5; ++kk) r5[kk] = radd(r5[kk], __shfl_xor_sync(0xffffffffu, r5[kk], off));
-        if (valid && (tau & 31) == 0) {
-          double* dst = a.abft.sig_part + (sig * NWS + (tau >> 5)) * 5;
+          for (int i = 0; i < 2; ++i) {
+            const T send = h3 ? s4[i] : s4[i + 2];
+            const T keep = h3 ? s4[i + 2] : s4[i];
+            s2[i] = radd(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+          }
+          T s1;
+          {
+            const T send = h2 ? s2[0] : s2[1];
+            const T keep = h2 ? s2[1] : s2[0];
+            s1 = radd(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+          }
+          s1 = radd(s1, __shfl_xor_sync(0xffffffffu, s1, 2));
+          s1 = radd(s1, __shfl_xor_sync(0xffffffffu, s1, 1));
+          const int idx = (h4 ? 4 : 0) + (h3 ? 2 : 0) + (h2 ? 1 : 0);
+          if (valid && (ln & 3) == 0 && idx < 5)
+            a.abft.sig_part[(sig * NWS + (tau >> 5)) * 5 + idx] = (double)s1;
+        } else {
+          T r5[5] = {(T)red5[0], (T)red5[1], (T)red5[2], (T)red5[3], (T)red5[4]};
 #pragma unroll
-          for (int kk = 0; kk < 5; ++kk) dst[kk] = (double)r5[kk];
+          for (int off = W0 / 2; off >= 1; off >>= 1)
+#pragma unroll
+            for (int kk = 0; kk < 5; ++kk) r5[kk] = radd(r5[kk], __shfl_xor_sync(0xffffffffu, r5[kk], off));
+          if (valid && (tau & 31) == 0) {
+            double* dst = a.abft.sig_part + (sig * NWS + (tau >> 5)) * 5;
+#pragma unroll
+            for (int kk = 0; kk < 5; ++kk) dst[kk] = (double)r5[kk];
+          }
         }
       }
     }
