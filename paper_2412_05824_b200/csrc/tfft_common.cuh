@@ -33,11 +33,55 @@ template <typename T> __device__ __forceinline__ C<T> csub(C<T> a, C<T> b) { ret
 template <typename T> __device__ __forceinline__ C<T> cmul(C<T> a, C<T> b) {
   return mk<T>(rfma(a.x, b.x, -rmul(a.y, b.y)), rfma(a.x, b.y, rmul(a.y, b.x)));
 }
+
+// FP32 complex arithmetic on the packed f32x2 pipe of sm_100 (FADD2 / FMUL2 /
+// FFMA2: both lanes in one instruction, operand swaps, broadcasts and per-lane
+// negation folded into the operands): half the FP32 instructions of the
+// scalar forms, with the same roundings per component, so every result is
+// bitwise the scalar version's.
+#define TFFT_F2(v) "f"(v.x), "f"(v.y)
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : TFFT_F2(a), TFFT_F2(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : TFFT_F2(a), TFFT_F2(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : TFFT_F2(a), TFFT_F2(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : TFFT_F2(a), TFFT_F2(b), TFFT_F2(c));
+  return r;
+}
+#undef TFFT_F2
+template <> __device__ __forceinline__ float2 cadd<float>(float2 a, float2 b) { return f2_add(a, b); }
+template <> __device__ __forceinline__ float2 csub<float>(float2 a, float2 b) { return f2_sub(a, b); }
+// t = (a.y b.y, a.y b.x) rounded; (a.x b.x - t.x, a.x b.y + t.y) in one fused op
+template <> __device__ __forceinline__ float2 cmul<float>(float2 a, float2 b) {
+  const float2 t = f2_mul(make_float2(a.y, a.y), make_float2(b.y, b.x));
+  return f2_fma(make_float2(a.x, a.x), b, make_float2(-t.x, t.y));
+}
 // multiply by -i (forward) or +i (inverse)
 template <typename T, bool INV> __device__ __forceinline__ C<T> rot90(C<T> a) {
   return INV ? mk<T>(-a.y, a.x) : mk<T>(a.y, -a.x);
 }
 template <typename T> __device__ __forceinline__ C<T> cscale(C<T> a, T s) { return mk<T>(rmul(a.x, s), rmul(a.y, s)); }
+template <> __device__ __forceinline__ float2 cscale<float>(float2 a, float s) { return f2_mul(a, make_float2(s, s)); }
 
 // ---------------------------------------------------------------------------
 // constant twiddles omega_R^k = exp(-+2 pi i k / R) for the in-register codelets
