@@ -80,8 +80,22 @@ template <> __device__ __forceinline__ float2 cmul<float>(float2 a, float2 b) {
 template <typename T, bool INV> __device__ __forceinline__ C<T> rot90(C<T> a) {
   return INV ? mk<T>(-a.y, a.x) : mk<T>(a.y, -a.x);
 }
+// acc + w x (checksum window sums) and acc + r v (checksum dot products),
+// one rounding per fused term; FP32: packed (FFMA2), same roundings per lane
+template <typename T> __device__ __forceinline__ C<T> caxpy(T w, C<T> x, C<T> acc) {
+  return mk<T>(rfma(w, x.x, acc.x), rfma(w, x.y, acc.y));
+}
+template <typename T> __device__ __forceinline__ C<T> cmac(C<T> r, C<T> v, C<T> acc) {
+  return mk<T>(rfma(r.x, v.x, rfma(-r.y, v.y, acc.x)), rfma(r.x, v.y, rfma(r.y, v.x, acc.y)));
+}
 template <typename T> __device__ __forceinline__ C<T> cscale(C<T> a, T s) { return mk<T>(rmul(a.x, s), rmul(a.y, s)); }
 template <> __device__ __forceinline__ float2 cscale<float>(float2 a, float s) { return f2_mul(a, make_float2(s, s)); }
+template <> __device__ __forceinline__ float2 caxpy<float>(float w, float2 x, float2 acc) {
+  return f2_fma(make_float2(w, w), x, acc);
+}
+template <> __device__ __forceinline__ float2 cmac<float>(float2 r, float2 v, float2 acc) {
+  return f2_fma(make_float2(r.x, r.x), v, f2_fma(make_float2(-r.y, r.y), make_float2(v.y, v.x), acc));
+}
 
 // ---------------------------------------------------------------------------
 // constant twiddles omega_R^k = exp(-+2 pi i k / R) for the in-register codelets

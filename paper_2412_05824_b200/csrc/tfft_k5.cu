@@ -126,7 +126,7 @@ __device__ __forceinline__ void tmem_axpy(uint32_t taddr, T w, const C<T> (&v)[E
     for (int q = 0; q < PER; ++q) {
       C<T> a = tw_get<T>(r, q);
       const C<T> x = v[ch * PER + q];
-      a = mk<T>(rfma(w, x.x, a.x), rfma(w, x.y, a.y));
+      a = caxpy<T>(w, x, a);
       tw_put(r, q, a);
     }
     tmem_st16(taddr + ch * 16, r);
@@ -312,13 +312,14 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
 #else
         tmem_read<T, E>(t_row, r);
 #endif
-        T cr = 0, cim = 0, fl = 0;
+        C<T> ci = mk<T>(0, 0);
+        T fl = 0;
 #pragma unroll
         for (int k = 0; k < E; ++k) {
-          cr = rfma(r[k].x, v[k].x, rfma(-r[k].y, v[k].y, cr));
-          cim = rfma(r[k].x, v[k].y, rfma(r[k].y, v[k].x, cim));
+          ci = cmac<T>(r[k], v[k], ci);
           fl = rfma(v[k].x, v[k].x, rfma(v[k].y, v[k].y, fl));
         }
+        const T cr = ci.x, cim = ci.y;
 #if !(TFFT_K5_EXP & 1)
         tmem_axpy<T, E>(t_sin, w, v);
 #endif
