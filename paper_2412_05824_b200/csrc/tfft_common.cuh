@@ -69,6 +69,7 @@ __device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
   return r;
 }
 #undef TFFT_F2
+#ifndef TFFT_NO_F32X2  // (experiment switch: the scalar forms)
 template <> __device__ __forceinline__ float2 cadd<float>(float2 a, float2 b) { return f2_add(a, b); }
 template <> __device__ __forceinline__ float2 csub<float>(float2 a, float2 b) { return f2_sub(a, b); }
 // t = (a.y b.y, a.y b.x) rounded; (a.x b.x - t.x, a.x b.y + t.y) in one fused op
@@ -76,6 +77,7 @@ template <> __device__ __forceinline__ float2 cmul<float>(float2 a, float2 b) {
   const float2 t = f2_mul(make_float2(a.y, a.y), make_float2(b.y, b.x));
   return f2_fma(make_float2(a.x, a.x), b, make_float2(-t.x, t.y));
 }
+#endif
 // multiply by -i (forward) or +i (inverse)
 template <typename T, bool INV> __device__ __forceinline__ C<T> rot90(C<T> a) {
   return INV ? mk<T>(-a.y, a.x) : mk<T>(a.y, -a.x);
@@ -89,6 +91,7 @@ template <typename T> __device__ __forceinline__ C<T> cmac(C<T> r, C<T> v, C<T> 
   return mk<T>(rfma(r.x, v.x, rfma(-r.y, v.y, acc.x)), rfma(r.x, v.y, rfma(r.y, v.x, acc.y)));
 }
 template <typename T> __device__ __forceinline__ C<T> cscale(C<T> a, T s) { return mk<T>(rmul(a.x, s), rmul(a.y, s)); }
+#ifndef TFFT_NO_F32X2
 template <> __device__ __forceinline__ float2 cscale<float>(float2 a, float s) { return f2_mul(a, make_float2(s, s)); }
 template <> __device__ __forceinline__ float2 caxpy<float>(float w, float2 x, float2 acc) {
   return f2_fma(make_float2(w, w), x, acc);
@@ -96,6 +99,7 @@ template <> __device__ __forceinline__ float2 caxpy<float>(float w, float2 x, fl
 template <> __device__ __forceinline__ float2 cmac<float>(float2 r, float2 v, float2 acc) {
   return f2_fma(make_float2(r.x, r.x), v, f2_fma(make_float2(-r.y, r.y), make_float2(v.y, v.x), acc));
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // constant twiddles omega_R^k = exp(-+2 pi i k / R) for the in-register codelets
