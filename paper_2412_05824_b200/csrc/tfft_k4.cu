@@ -466,7 +466,9 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       const unsigned mb = (unsigned)p * (unsigned)tA, ms = (unsigned)p * (unsigned)P::TPS;
       const CT bh = __ldg(hi + (mb >> LO)), bl = __ldg(lo + (mb & LOM));
       const CT sh = __ldg(hi + (ms >> LO)), sl_ = __ldg(lo + (ms & LOM));
+#if !(TFFT_K7_EXP & 2)  // experiment: K4 FFT arithmetic compiled out
       P::F::run(slots + P::base(gA), v, tA, tws1);
+#endif
       // blocked ring layout: Z'[p][q] at ((q / CB_B) * N2 + p) * CB_B + q % CB_B
       CT* d = z + ((cur.g % 3) * G + sl) * N + p * PB::CB;
       const CT step = cmul<T>(sh, sl_);
@@ -504,7 +506,9 @@ __global__ void __launch_bounds__(NT + 64, MINB)
         for (int i = tid; i < K::TILE * K::BPC / 128; i += NT)
           asm volatile("discard.global.L2 [%0], 128;" ::"l"(src + (int64_t)i * 128) : "memory");
       }
+#if !(TFFT_K7_EXP & 2)  // experiment: K4 FFT arithmetic compiled out
       P::F::run(slots + P::base(gB), v, tB, tws2);
+#endif
       const int sl = r / ncbB;
       const int q0 = (r - sl * ncbB) * P::CB;
       CT* d = y + (cur.g * G + sl) * N + q0 + gB;
