@@ -21,20 +21,22 @@ namespace tfft {
 
 // Single-column work of the replay runs at full width: CTA c owns the
 // 8192-element chunk c and writes its partials; a one-warp finisher combines
-// the chunks in order (deterministic). The partials live in a per-device
-// scratch (the replay is serial per device; 2^29 / 8192 chunks x 2 doubles).
+// the chunks in order (deterministic). The partials come from the stream-
+// ordered allocator (cudaMallocAsync / cudaFreeAsync on the caller's stream),
+// so calls on different streams never share them.
 constexpr int64_t kChunk = 8192;
 
-double* chunk_scratch() {
-  static double* buf[kMaxDevices] = {};
-  const int d = current_device();
-  if (!buf[d]) {
-    if (cudaMalloc(&buf[d], (size_t)((int64_t(1) << 29) / kChunk) * 2 * sizeof(double)) != cudaSuccess) {
-      buf[d] = nullptr;
-    }
+struct ChunkScratch {
+  double* p = nullptr;
+  cudaStream_t st;
+  ChunkScratch(int64_t n, cudaStream_t s) : st(s) {
+    const size_t bytes = (size_t)((n + kChunk - 1) / kChunk) * 2 * sizeof(double);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, st) != cudaSuccess) p = nullptr;
   }
-  return buf[d];
-}
+  ~ChunkScratch() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
 
 
 // ---------------------------------------------------------------------------
@@ -783,7 +785,8 @@ __global__ void __launch_bounds__(256) group_div_kernel(const C<T>* ref, const C
 
 int launch_group_div(int prec, const void* ref, const void* s_out, int64_t n, double* out, cudaStream_t st) {
   if (n >= 65536) {  // one long row: chunk partials at full width, combined in order
-    double* part = chunk_scratch();
+    ChunkScratch scratch(n, st);
+    double* part = scratch.p;
     if (!part) return (int)cudaErrorMemoryAllocation;
     return launch_group_div_chunked(prec, ref, s_out, n, 1, out, part, st);
   }
@@ -926,7 +929,8 @@ __global__ void chunk_finish_kernel(const double* part, int64_t nchunk, int mode
 // the column is (snap_out - ref) / w with ref in the same precision.
 int launch_correction_column(int prec, const void* snap_out, const void* ref64, int64_t n, double weight, void* col,
                              double* res, cudaStream_t st) {
-  double* part = chunk_scratch();
+  ChunkScratch scratch(n, st);
+  double* part = scratch.p;
   if (!part) return (int)cudaErrorMemoryAllocation;
   const int64_t nc = (n + kChunk - 1) / kChunk;
   if (prec == 0)
@@ -960,7 +964,8 @@ __global__ void __launch_bounds__(256) patch_row_kernel(C<T>* yk, const C<T>* co
 
 int launch_patch_row(int prec, void* yk, const void* col, int64_t n, int enc, const void* tw, double* res,
                      cudaStream_t st) {
-  double* part = chunk_scratch();
+  ChunkScratch scratch(n, st);
+  double* part = scratch.p;
   if (!part) return (int)cudaErrorMemoryAllocation;
   const int64_t nc = (n + kChunk - 1) / kChunk;
   if (prec == 0)
