@@ -750,15 +750,14 @@ def _batched_windows(plan, source, y, batch, txs, ntx, nwin, T, div, host, kind,
     weights = np.asarray(run.state.weights, dtype=np.float64)
     starts = np.array([meta[i][1].start for i in done])
     sizes = np.array([meta[i][1].stop - meta[i][1].start for i in done])
-    tx_res = np.zeros(len(done), dtype=np.complex128)
-    tx_wres = np.zeros(len(done), dtype=np.complex128)
     with np.errstate(over="ignore", invalid="ignore"):
-        for j in range(int(sizes.max())):
-            live = j < sizes
-            idx = np.where(live, starts + j, starts)
-            r = np.where(live, c_in[idx] - c_out[idx], 0)
-            tx_res = tx_res + r
-            tx_wres = tx_wres + np.where(live, weights[idx], 0.0) * r
+        cols = np.arange(int(sizes.max()))
+        live = cols[None, :] < sizes[:, None]
+        idx = np.where(live, starts[:, None] + cols[None, :], starts[:, None])
+        r = np.where(live, c_in[idx] - c_out[idx], 0)
+        # cumulative sums run left to right: the sequential order of sum()
+        tx_res = np.cumsum(r, axis=1)[:, -1]
+        tx_wres = np.cumsum(np.where(live, weights[idx], 0.0) * r, axis=1)[:, -1]
         for q, i in enumerate(done):
             w, tx, k = meta[i]
             try:
