@@ -405,7 +405,7 @@ def _kernel_label(prec, n):
     if logn <= (13 if prec == "single" else 12):
         return "k5_single_pass"
     if logn <= 22:
-        return ("k7" if prec == "double" and logn <= 20 else "k4/k3") + "_two_pass"
+        return ("k7" if logn <= 20 else "k4/k3") + "_two_pass"
     return "stage_passes"
 
 

@@ -101,6 +101,29 @@ template <> __device__ __forceinline__ float2 cmac<float>(float2 r, float2 v, fl
 }
 #endif
 
+// Twiddle run w_j = base * step^j, j = 0, 1, ... in ascending order, as four
+// interleaved product chains (w_{j+4} = w_j * step^4): a dependency depth of
+// about j/4 + 2 complex products instead of the j of the single recurrence,
+// which left the four-step twiddle epilogues latency-bound. next(j) returns
+// w_j and must be called with j = 0, 1, 2, ... (unrolled, compile-time j).
+template <typename T>
+struct TwRun {
+  C<T> c[4], s4;
+  __device__ __forceinline__ TwRun(C<T> base, C<T> step) {
+    const C<T> s2 = cmul<T>(step, step);
+    c[0] = base;
+    c[1] = cmul<T>(base, step);
+    c[2] = cmul<T>(base, s2);
+    c[3] = cmul<T>(c[1], s2);
+    s4 = cmul<T>(s2, s2);
+  }
+  __device__ __forceinline__ C<T> next(int j) {
+    const C<T> w = c[j & 3];
+    c[j & 3] = cmul<T>(c[j & 3], s4);
+    return w;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // constant twiddles omega_R^k = exp(-+2 pi i k / R) for the in-register codelets
 

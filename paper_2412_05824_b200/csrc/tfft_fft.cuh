@@ -45,7 +45,12 @@ __device__ __forceinline__ void fft_sync_grp(int bar_id) {
 //          pass P's block holds w_{S R}^{q t} at (t - 1) * S + q, q fastest, so
 //          the lanes of a warp (consecutive q) read consecutive words: no bank
 //          conflicts, unlike strided reads of a w_N copy (up to 8-way).
-template <typename T, int N_, int E_, bool INV, bool PF = false, int BAR_THREADS = 0, bool TWS = false>
+// TWG (with TWS): per leg group, load only w^1 (and w^4, w^8, w^12 at radix
+//          8/16) of a pass's table and form the other powers by one or two
+//          complex products: 4 instead of 15 shared-memory twiddle reads per
+//          radix-16 group, for kernels whose shared-memory pipe is the limiter.
+template <typename T, int N_, int E_, bool INV, bool PF = false, int BAR_THREADS = 0, bool TWS = false,
+          bool TWG = false>
 struct Fft {
   static constexpr int N = N_;
   static constexpr int E = (E_ < N_) ? E_ : N_;
@@ -112,6 +117,27 @@ struct Fft {
 #pragma unroll
       for (int u = 0; u < E / R; ++u) {
         const int q = (tau + TPS * u) & (S - 1);
+        if constexpr (TWG && TWS && R >= 4) {
+          const C<T>* b = tw + pass_off<P>() + q;  // w^t at b[(t - 1) * S]
+          w[u * R + 1] = b[0];
+          w[u * R + 2] = cmul<T>(w[u * R + 1], w[u * R + 1]);
+          w[u * R + 3] = cmul<T>(w[u * R + 2], w[u * R + 1]);
+          if constexpr (R >= 8) {
+            w[u * R + 4] = b[3 * S];
+#pragma unroll
+            for (int t = 1; t < 4; ++t) w[u * R + 4 + t] = cmul<T>(w[u * R + 4], w[u * R + t]);
+          }
+          if constexpr (R == 16) {
+            w[u * R + 8] = b[7 * S];
+            w[u * R + 12] = b[11 * S];
+#pragma unroll
+            for (int t = 1; t < 4; ++t) {
+              w[u * R + 8 + t] = cmul<T>(w[u * R + 8], w[u * R + t]);
+              w[u * R + 12 + t] = cmul<T>(w[u * R + 12], w[u * R + t]);
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int t = 1; t < R; ++t) {
           if constexpr (TWS) w[u * R + t] = tw[pass_off<P>() + (t - 1) * S + q];

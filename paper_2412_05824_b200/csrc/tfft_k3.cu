@@ -162,13 +162,10 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT, MODE == 2 ? TFFT_COL2_MIN
         const int64_t scale = a.n / (a.s * L);
         const int64_t mb = (q * (int64_t)tau * scale) & (a.n - 1);
         const int64_t ms = (q * (int64_t)TPS * scale) & (a.n - 1);
-        CT w = cmul<T>(__ldg(hi + (mb >> a.lo_bits)), __ldg(lo + (mb & lomask)));
-        const CT step = cmul<T>(__ldg(hi + (ms >> a.lo_bits)), __ldg(lo + (ms & lomask)));
+        TwRun<T> w(cmul<T>(__ldg(hi + (mb >> a.lo_bits)), __ldg(lo + (mb & lomask))),
+                   cmul<T>(__ldg(hi + (ms >> a.lo_bits)), __ldg(lo + (ms & lomask))));
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          v[k] = cmul<T>(v[k], w);
-          if (k + 1 < E) w = cmul<T>(w, step);
-        }
+        for (int k = 0; k < E; ++k) v[k] = cmul<T>(v[k], w.next(k));
       }
     }
     F::run(slot, v, tau, tw);
@@ -515,12 +512,9 @@ __global__ void __launch_bounds__(ColCfg<T, LOGL>::NT) stage_abft_kernel(ColArgs
         }
       }
       if constexpr (PH == 2) {
-        CT wv = tw0;
+        TwRun<T> wv(tw0, tstep);
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          v[k] = cmul<T>(v[k], wv);
-          if (k + 1 < E) wv = cmul<T>(wv, tstep);
-        }
+        for (int k = 0; k < E; ++k) v[k] = cmul<T>(v[k], wv.next(k));
       }
       F::run(slot, v, tau, tw);
       if constexpr (PH == 0) {
@@ -892,6 +886,11 @@ bool k3_strikes_stage1(const K3Plan* p) { return p && p->stage1; }
 int k3_launches(const K3Plan* p) { return p && p->k4 ? 1 : 2; }
 
 // K4 group size: ~16 MB of intermediate per group, so the 3-slot ring is ~48 MB
+// the plain two-pass schedule runs on K7 (else K4)
+static bool k7_on(const K3Plan* p) {
+  return k7_supported(p->prec, p->l1, p->l2) && std::getenv("TFFT_NO_K7") == nullptr;
+}
+
 static int64_t k4_group(const K3Plan* p, int64_t batch) {
   const int64_t cb = p->prec == 0 ? 8 : 16;
   // ~16 MB of intermediate per group (3-slot ring ~48 MB) up to 2^16; 32 MB
@@ -970,7 +969,10 @@ static int k4_execute_chunk(K3Plan* p, const void* x, void* y, int64_t batch, in
     p->ring_cap = ring;
   }
   const int64_t ng = (batch + G - 1) / G;
-  const size_t sync = 8 + (size_t)2 * ng * sizeof(unsigned);
+  const bool k7 = k7_on(p);
+  const bool ldisc = k7 && k7_line_discard(p->prec, p->l1, p->l2) && std::getenv("TFFT_K7_LDISC") != nullptr;
+  const size_t lcnt = ldisc ? (size_t)batch * ((int64_t(1) << p->l1) / (p->prec == 0 ? 16 : 8)) : 0;
+  const size_t sync = 8 + ((size_t)2 * ng + lcnt) * sizeof(unsigned);
   if (p->sync_cap < sync) {
     cudaFree(p->sync);
     p->sync = nullptr;
@@ -983,8 +985,9 @@ static int k4_execute_chunk(K3Plan* p, const void* x, void* y, int64_t batch, in
   if (e != cudaSuccess) return (int)e;
   const int64_t N1 = int64_t(1) << p->l1, N2 = int64_t(1) << p->l2;
   const int lmax = p->l1 > p->l2 ? p->l1 : p->l2;
-  const int64_t tpa = N2 / k4_columns_per_tile(p->prec, p->l1, lmax);  // pass-A tiles per signal
-  const int64_t tpb = N1 / k4_columns_per_tile(p->prec, p->l2, lmax);
+  // pass-A / pass-B tiles per signal
+  const int64_t tpa = N2 / (k7 ? k7_columns_per_tile(p->prec, p->l1) : k4_columns_per_tile(p->prec, p->l1, lmax));
+  const int64_t tpb = N1 / (k7 ? k7_columns_per_tile(p->prec, p->l2) : k4_columns_per_tile(p->prec, p->l2, lmax));
   const int64_t glast = batch - (ng - 1) * G;
   const int c = inverse ? 1 : 0;
   K4Args a{};
@@ -1010,8 +1013,9 @@ static int k4_execute_chunk(K3Plan* p, const void* x, void* y, int64_t batch, in
   a.ticket = static_cast<unsigned long long*>(p->sync);
   a.done_a = reinterpret_cast<unsigned*>(static_cast<char*>(p->sync) + 8);
   a.done_b = a.done_a + ng;
-  if (p->prec == 1 && k7_supported(p->l1, p->l2) && std::getenv("TFFT_NO_K7") == nullptr)
-    return launch_k7(inverse != 0, p->l1, p->l2, a, p->num_sms, st);
+  a.line_cnt = ldisc ? a.done_b + ng : nullptr;
+  if (k7)
+    return launch_k7(p->prec, inverse != 0, p->l1, p->l2, a, p->num_sms, st);
   return launch_k4(p->prec, inverse != 0, p->l1, p->l2, a, p->num_sms, st);
 }
 
@@ -1068,8 +1072,7 @@ int k3_execute(K3Plan* p, const void* x, void* y, int64_t batch, int inverse, co
 int k3_protected(K3Plan* p, const void* x, void* y, int64_t batch, int64_t weight0, const DevFault* faults,
                  int nfaults, Counters* counters, const AbftArgs& ab, const void* row, void* s_in, void* s_out,
                  double* sig_part, int64_t* nparts, cudaStream_t st) {
-  if (!p->k4 || (p->prec == 1 && k7_supported(p->l1, p->l2) && std::getenv("TFFT_NO_K7") == nullptr))
-    return (int)cudaErrorNotSupported;
+  if (!p->k4 || k7_on(p)) return (int)cudaErrorNotSupported;
   if (ab.enc != ENC_WANG && ab.enc != ENC_ONES) return (int)cudaErrorNotSupported;
   const int64_t W = ab.win_signals;
   const int64_t G0 = k4_group(p, batch);

@@ -471,8 +471,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
 #endif
       // blocked ring layout: Z'[p][q] at ((q / CB_B) * N2 + p) * CB_B + q % CB_B
       CT* d = z + ((cur.g % 3) * G + sl) * N + p * PB::CB;
-      const CT step = cmul<T>(sh, sl_);
-      CT w = cmul<T>(bh, bl);  // running w_N^{p (tA + TPS j)}, j ascending (<= E-1 products)
+      TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));  // w_N^{p (tA + TPS j)}, j ascending
       const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
 #pragma unroll
       for (int j = 0; j < E; ++j) {
@@ -488,8 +487,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
             }
           }
         }
-        d[(q / PB::CB) * (N2 * PB::CB) + (q % PB::CB)] = cmul<T>(v[k], w);
-        if (j + 1 < E) w = cmul<T>(w, step);
+        d[(q / PB::CB) * (N2 * PB::CB) + (q % PB::CB)] = cmul<T>(v[k], w.next(j));
       }
     } else {
       using P = PB;
@@ -607,35 +605,51 @@ static int launch_k4_abft_t(const K4Args& a, int num_sms, cudaStream_t st) {
 //  * pass-B outputs are staged in a swizzled [row k][column] buffer and leave
 //    by one set of 2-D TMA stores per tile (one consumer barrier pair per B
 //    tile).
-template <int LOGL, bool INV>
+#ifndef TFFT_K7_TWG
+#define TFFT_K7_TWG 1
+#endif
+#ifndef TFFT_K7F_NT
+#define TFFT_K7F_NT 256
+#endif
+template <typename T, int LOGL, bool INV, int NT_>
 struct K7Ph {
+  using CT = C<T>;
+  static constexpr int ES = sizeof(CT);  // bytes per complex element
   static constexpr int L = 1 << LOGL;
-  using F = Fft<double, L, 16, INV, false, -1, true>;
+  using F = Fft<T, L, 16, INV, false, -1, true, TFFT_K7_TWG != 0>;
   static constexpr int TPS = F::TPS;
-  static constexpr int NT = 128;
+  static constexpr int NT = NT_;
   static constexpr int CB = NT / TPS;
   static_assert(TPS <= 64 && CB * TPS == NT, "warp-local columns (two warps at 1024 points)");
-  static constexpr int BW = CB < 8 ? CB : 8;  // columns per TMA box (<= 128 B rows)
-  static constexpr int MASK = BW == 8 ? 7 : (BW == 4 ? 3 : (BW == 2 ? 1 : 0));
+  static constexpr int LINE = 128 / ES;                 // elements per 128-byte line
+  static constexpr int BW = CB < LINE ? CB : LINE;      // columns per TMA box (<= 128 B rows)
+  static constexpr int RB = BW * ES;                    // box row bytes
+  static_assert(RB >= 16, "TMA rows of at least 16 bytes");
+  static constexpr int MASK = RB == 128 ? 7 : (RB == 64 ? 3 : (RB == 32 ? 1 : 0));
   static constexpr CUtensorMapSwizzle SWZ =
-      BW == 8 ? CU_TENSOR_MAP_SWIZZLE_128B
-              : (BW == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : (BW == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE));
+      RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                : (RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : (RB == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE));
   static constexpr int BOXR = L < 256 ? L : 256;
   static constexpr int NBOX = L / BOXR;
   // element (row r, column c) of a staged tile, as placed by the swizzled TMA
+  // (the swizzle permutes the 16-byte chunks of each 128-byte span)
   static __device__ __forceinline__ int sidx(int r, int c) {
-    const int off = (r * BW + (c % BW)) * 16;
-    return (c / BW) * (L * BW) + ((off ^ (((off >> 7) & MASK) << 4)) >> 4);
+    const int off = (r * BW + (c % BW)) * ES;
+    return (c / BW) * (L * BW) + (off ^ (((off >> 7) & MASK) << 4)) / ES;
   }
   static constexpr int SLOTQ = (F::NPAD + 7) / 8 * 8 + (TPS < 8 ? TPS : 0);
   static constexpr int ELEMS = CB * SLOTQ;
 };
 
-template <int L1, int L2, bool INV>
+template <typename T>
+struct K7Nt { static constexpr int NT = sizeof(T) == 4 ? TFFT_K7F_NT : 128; };
+
+template <typename T, int L1, int L2, bool INV>
 struct K7Cfg {
-  using PA = K7Ph<L1, INV>;
-  using PB = K7Ph<L2, INV>;
-  static constexpr int NT = 128;
+  static constexpr int NT = K7Nt<T>::NT;
+  using PA = K7Ph<T, L1, INV, NT>;
+  using PB = K7Ph<T, L2, INV, NT>;
+  static constexpr int ES = PA::ES;
   static constexpr int TILE = NT * 16;
   static constexpr int SLOTS = PA::ELEMS > PB::ELEMS ? PA::ELEMS : PB::ELEMS;
   static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));
@@ -646,9 +660,10 @@ struct K7Cfg {
   // (1024-point columns only: at <= 512 points a separate staging buffer still
   // fits two CTAs per SM and saves the wait for the stores' smem reads)
   static constexpr bool ALIAS = L1 >= 10 || L2 >= 10;
-  static constexpr int SLOTS_AL = (SLOTS * 16 > TILE * 16 ? SLOTS : TILE);
-  static constexpr int SLOTS_SZ = (SLOTS_AL + 63) / 64 * 64;
-  static constexpr int SMEM = (TILE + (ALIAS ? 0 : TILE) + SLOTS_SZ + TWE) * 16 + 16 + RR * 24 + 1024 + 256;
+  static constexpr int SLOTS_AL = (SLOTS > TILE ? SLOTS : TILE);
+  static constexpr int AL = 1024 / ES;  // 1024-byte alignment of the swizzled regions
+  static constexpr int SLOTS_SZ = (SLOTS_AL + AL - 1) / AL * AL;
+  static constexpr int SMEM = (TILE + (ALIAS ? 0 : TILE) + SLOTS_SZ + TWE) * ES + 16 + RR * 24 + 1024 + 256;
 };
 
 __device__ __forceinline__ void k7_tma_store(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -658,14 +673,14 @@ __device__ __forceinline__ void k7_tma_store(const CUtensorMap* map, const void*
                : "memory");
 }
 
-template <int L1, int L2, bool INV>
-__global__ void __launch_bounds__(192, 2)
+template <typename T, int L1, int L2, bool INV>
+__global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
     k7_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmz,
               const __grid_constant__ CUtensorMap tmy, K4Args a) {
-  using K = K7Cfg<L1, L2, INV>;
+  using K = K7Cfg<T, L1, L2, INV>;
   using PA = typename K::PA;
   using PB = typename K::PB;
-  using CT = double2;
+  using CT = C<T>;
   constexpr int NT = K::NT;
   constexpr int N1 = 1 << L1, N2 = 1 << L2;
   constexpr int64_t N = int64_t(N1) * N2;
@@ -703,8 +718,15 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
 
   if (tid >= NT + 32) {
-    // releaser (as K4)
-    if (tid != NT + 32) return;
+    // releaser (as K4). Pass-B tiles narrower than a 128-byte ring line
+    // (CB_B < LINE columns) cannot discard their lines themselves: the 8 / CB_B
+    // tiles sharing a line group count in a.line_cnt and the releaser of the
+    // last one drops the group's N2 lines from L2 without write-back (the
+    // consumers discard whole-line tiles themselves), before publishing the
+    // tile, so pass A of group g + 3 rewrites the slot only after the discard.
+    constexpr bool LDISC = PB::CB < PB::LINE;
+    if (!LDISC && tid != NT + 32) return;
+    const int lane = tid & 31;
 #pragma unroll 1
     for (int it = 0;; ++it) {
       const int i = it % K::RR;
@@ -712,6 +734,23 @@ __global__ void __launch_bounds__(192, 2)
       const long long t = rtk[i];
       if (t < 0) return;
       const K4Item c = k4_decode(a, t);
+      if constexpr (LDISC) {
+        if (c.phase == 1 && a.line_cnt != nullptr) {
+          constexpr int TPL = PB::LINE / PB::CB;  // tiles per line group
+          const int64_t sl = c.r / ncbB;
+          const int lg = (int)(c.r - sl * ncbB) / TPL;
+          unsigned last = 0;
+          if (lane == 0) last = atomicAdd(a.line_cnt + (c.g * G + sl) * (N1 / PB::LINE) + lg, 1u) == TPL - 1;
+          if (__shfl_sync(0xffffffffu, last, 0)) {
+            const CT* base = static_cast<const CT*>(a.z) + ((c.g % 3) * G + sl) * N + lg * PB::LINE;
+#pragma unroll 4
+            for (int p = lane; p < N2; p += 32)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (int64_t)p * N1) : "memory");
+          }
+        }
+        __syncwarp();
+        if (lane != 0) continue;
+      }
       red_release_add(c.phase == 0 ? a.done_a + c.g : a.done_b + c.g, 1u);
       mbar_arrive(&relfree[i]);
     }
@@ -737,7 +776,7 @@ __global__ void __launch_bounds__(192, 2)
       }
       tk[0] = t;
       const int r = (int)item.r;
-      mbar_expect_tx(&full[0], K::TILE * 16);
+      mbar_expect_tx(&full[0], K::TILE * K::ES);
       if (item.phase == 0) {
         using P = PA;
         const int sl = r / ncbA;
@@ -800,7 +839,7 @@ __global__ void __launch_bounds__(192, 2)
       const int64_t sig = cur.g * G + sl;
       const int p = (r - sl * ncbA) * P::CB + g;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) bad |= !finite2<double>(v[k]);
+      for (int k = 0; k < 16; ++k) bad |= !finite2<T>(v[k]);
       if (a.nfaults > 0) {
         for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
           const DevFault fl = a.faults[f];
@@ -828,8 +867,7 @@ __global__ void __launch_bounds__(192, 2)
       P::F::run(slots + g * P::SLOTQ, v, tau, tws1, 2 + g);
 #endif
       CT* d = z + ((cur.g % 3) * G + sl) * N + (int64_t)p * N1;  // p-major ring
-      const CT step = cmul<double>(sh, sl_);
-      CT w = cmul<double>(bh, bl);
+      TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));
       const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -845,8 +883,7 @@ __global__ void __launch_bounds__(192, 2)
             }
           }
         }
-        d[q] = cmul<double>(v[k], w);
-        if (j + 1 < 16) w = cmul<double>(w, step);
+        d[q] = cmul<T>(v[k], w.next(j));
       }
     } else {
       using P = PB;
@@ -857,15 +894,16 @@ __global__ void __launch_bounds__(192, 2)
       if ((tid & 31) == 0) mbar_arrive(&empty[0]);
       {
         // the tile's ring lines are dead: CB_B columns of N2 rows, 128-byte
-        // lines hold 8 columns, so only whole-line tiles (CB_B >= 8) discard
-        if constexpr (P::CB >= 8) {
+        // lines hold LINE columns, so only whole-line tiles (CB_B >= LINE) discard
+        if constexpr (P::CB >= P::LINE) {
+          constexpr int LPR = P::CB / P::LINE;  // lines per ring row of the tile
           const int sl = r / ncbB;
           const int q0 = (r - sl * ncbB) * P::CB;
           const CT* base = z + ((cur.g % 3) * G + sl) * N + q0;
 #pragma unroll 1
-          for (int i = tid; i < N2 * (P::CB / 8); i += NT)
-            asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (int64_t)(i / (P::CB / 8)) * N1 +
-                                                               (i % (P::CB / 8)) * 8)
+          for (int i = tid; i < N2 * LPR; i += NT)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (int64_t)(i / LPR) * N1 +
+                                                               (i % LPR) * P::LINE)
                          : "memory");
         }
       }
@@ -884,7 +922,7 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         CT val = v[k];
-        if constexpr (INV) val = cscale<double>(val, 1.0 / (double)N);
+        if constexpr (INV) val = cscale<T>(val, (T)(1.0 / (double)N));
         ystage[P::sidx(tau + P::TPS * P::F::out_pos(k), g)] = val;
       }
       fence_proxy_async();
@@ -910,17 +948,17 @@ __global__ void __launch_bounds__(192, 2)
   if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
 }
 
-template <int L1, int L2, bool INV>
+template <typename T, int L1, int L2, bool INV>
 static int launch_k7_t(const K4Args& a, int num_sms, cudaStream_t st) {
-  using K = K7Cfg<L1, L2, INV>;
-  auto kern = k7_kernel<L1, L2, INV>;
+  using K = K7Cfg<T, L1, L2, INV>;
+  auto kern = k7_kernel<T, L1, L2, INV>;
   static LaunchCfg cfg;
   const int dev = current_device();
   if (!cfg.done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     if (e != cudaSuccess) return (int)e;
     int ps = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 192, K::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, K::NT + 64, K::SMEM);
     if (e != cudaSuccess) return (int)e;
     cfg.per_sm[dev] = ps < 1 ? 1 : ps;
     cfg.done[dev] = true;
@@ -931,25 +969,28 @@ static int launch_k7_t(const K4Args& a, int num_sms, cudaStream_t st) {
   if (grid > total) grid = total;
   if (grid < 1) return 0;
   CUtensorMap tmx, tmz, tmy;
-  const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  constexpr uint64_t es = K::ES;
   // x: (B N1) rows of N2; ring: (3 G N2) rows of N1 (p-major); y: (B N2) rows of N1
   int rc = k4_encode_2d(&tmx, dt, const_cast<void*>(a.x), (uint64_t)(2 << L2), (uint64_t)a.batch << L1,
-                        (uint64_t)16 << L2, (uint32_t)(2 * K::PA::BW), (uint32_t)K::PA::BOXR, K::PA::SWZ);
+                        es << L2, (uint32_t)(2 * K::PA::BW), (uint32_t)K::PA::BOXR, K::PA::SWZ);
   if (!rc)
-    rc = k4_encode_2d(&tmz, dt, a.z, (uint64_t)(2 << L1), (uint64_t)(3 * a.group) << L2, (uint64_t)16 << L1,
+    rc = k4_encode_2d(&tmz, dt, a.z, (uint64_t)(2 << L1), (uint64_t)(3 * a.group) << L2, es << L1,
                       (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
   if (!rc)
-    rc = k4_encode_2d(&tmy, dt, a.y, (uint64_t)(2 << L1), (uint64_t)a.batch << L2, (uint64_t)16 << L1,
+    rc = k4_encode_2d(&tmy, dt, a.y, (uint64_t)(2 << L1), (uint64_t)a.batch << L2, es << L1,
                       (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
   if (rc) return rc;
-  kern<<<(unsigned)grid, 192, K::SMEM, st>>>(tmx, tmz, tmy, a);
+  kern<<<(unsigned)grid, K::NT + 64, K::SMEM, st>>>(tmx, tmz, tmy, a);
   return (int)cudaGetLastError();
 }
 
 #define TFFT_K7_PAIRS \
   TFFT_K4(7, 6) TFFT_K4(7, 7) TFFT_K4(8, 7) TFFT_K4(8, 8) TFFT_K4(8, 9) TFFT_K4(9, 9) TFFT_K4(10, 9) TFFT_K4(10, 10)
 
-bool k7_supported(int l1, int l2) {
+// K7 runs FP64 2^13..2^20 and FP32 2^14..2^20 (FP32 2^13 is single-pass K5)
+bool k7_supported(int prec, int l1, int l2) {
+  if (prec == 0 && l1 + l2 < 14) return false;
 #define TFFT_K4(A, B) \
   if (l1 == A && l2 == B) return true;
   TFFT_K7_PAIRS
@@ -957,12 +998,29 @@ bool k7_supported(int l1, int l2) {
   return false;
 }
 
-int launch_k7(bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
+int k7_columns_per_tile(int prec, int logl) {
+  const int tps = (1 << logl) / 16;
+  return (prec == 0 ? K7Nt<float>::NT : K7Nt<double>::NT) / tps;
+}
+
+bool k7_line_discard(int prec, int l1, int l2) {
+  (void)l1;
+  return k7_columns_per_tile(prec, l2) < (prec == 0 ? 16 : 8);
+}
+
+template <typename T>
+static int dispatch_k7(bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
 #define TFFT_K4(A, B) \
-  if (l1 == A && l2 == B) return inverse ? launch_k7_t<A, B, true>(a, num_sms, st) : launch_k7_t<A, B, false>(a, num_sms, st);
+  if (l1 == A && l2 == B)  \
+    return inverse ? launch_k7_t<T, A, B, true>(a, num_sms, st) : launch_k7_t<T, A, B, false>(a, num_sms, st);
   TFFT_K7_PAIRS
 #undef TFFT_K4
   return (int)cudaErrorInvalidValue;
+}
+
+int launch_k7(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st) {
+  if (prec == 0) return dispatch_k7<float>(inverse, l1, l2, a, num_sms, st);
+  return dispatch_k7<double>(inverse, l1, l2, a, num_sms, st);
 }
 
 // (FP32: 128-consumer CTAs measured faster up to 256-point columns, 256 beyond)

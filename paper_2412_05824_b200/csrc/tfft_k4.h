@@ -37,6 +37,7 @@ struct K4Args {
   unsigned long long* ticket;  // zeroed before the launch
   unsigned* done_a;      // [ngroups] finished pass-A tiles, zeroed before the launch
   unsigned* done_b;      // [ngroups]
+  unsigned* line_cnt;    // K7: [batch][N1/8] finished pass-B tiles per ring line group (null: no discards)
   // ---- fused two-sided ABFT (K4 only; abft = 0: plain transform). After the
   // B tiles of each group come its C tiles: (window, position chunk) items
   // that read x and y of the window's signals while they are still in L2 and
@@ -63,7 +64,11 @@ int k4_abft_chunk(int prec, int l1, int l2);
 int launch_k4_abft(int prec, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
 // K7: FP64 K4 variant with warp-local columns (columns <= 512 points); the
 // intermediate ring is p-major instead of K4's column-blocked layout
-bool k7_supported(int l1, int l2);
-int launch_k7(bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
+bool k7_supported(int prec, int l1, int l2);
+// pass-A / pass-B columns per K7 tile
+int k7_columns_per_tile(int prec, int logl);
+// pass-B tiles narrower than a ring line: line groups discarded by the releaser (K4Args::line_cnt)
+bool k7_line_discard(int prec, int l1, int l2);
+int launch_k7(int prec, bool inverse, int l1, int l2, const K4Args& a, int num_sms, cudaStream_t st);
 
 }  // namespace tfft

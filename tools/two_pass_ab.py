@@ -1,4 +1,4 @@
-"""Time the plain two-pass transforms (K7 FP64 / K4 FP32) over 1 GiB inputs for
+"""Time the plain two-pass transforms (K7; K4 at FP32 2^21..2^22) over 1 GiB inputs for
 a list of log2 N (env TP_LOGN), CUDA events, 10 reps after 3 warm-ups."""
 import os
 import sys
