@@ -605,18 +605,20 @@ static int launch_k4_abft_t(const K4Args& a, int num_sms, cudaStream_t st) {
 //  * pass-B outputs are staged in a swizzled [row k][column] buffer and leave
 //    by one set of 2-D TMA stores per tile (one consumer barrier pair per B
 //    tile).
+// generated radix-16 twiddles (Fft TWG): 1-3% faster at every split but
+// (9, 9), 3% slower there
 #ifndef TFFT_K7_TWG
-#define TFFT_K7_TWG 1
+#define TFFT_K7_TWG -1
 #endif
 #ifndef TFFT_K7F_NT
 #define TFFT_K7F_NT 256
 #endif
-template <typename T, int LOGL, bool INV, int NT_>
+template <typename T, int LOGL, bool INV, int NT_, bool TWG>
 struct K7Ph {
   using CT = C<T>;
   static constexpr int ES = sizeof(CT);  // bytes per complex element
   static constexpr int L = 1 << LOGL;
-  using F = Fft<T, L, 16, INV, false, -1, true, TFFT_K7_TWG != 0>;
+  using F = Fft<T, L, 16, INV, false, -1, true, TWG>;
   static constexpr int TPS = F::TPS;
   static constexpr int NT = NT_;
   static constexpr int CB = NT / TPS;
@@ -647,8 +649,9 @@ struct K7Nt { static constexpr int NT = sizeof(T) == 4 ? TFFT_K7F_NT : 128; };
 template <typename T, int L1, int L2, bool INV>
 struct K7Cfg {
   static constexpr int NT = K7Nt<T>::NT;
-  using PA = K7Ph<T, L1, INV, NT>;
-  using PB = K7Ph<T, L2, INV, NT>;
+  static constexpr bool TWG = TFFT_K7_TWG < 0 ? !(L1 == 9 && L2 == 9) : TFFT_K7_TWG != 0;
+  using PA = K7Ph<T, L1, INV, NT, TWG>;
+  using PB = K7Ph<T, L2, INV, NT, TWG>;
   static constexpr int ES = PA::ES;
   static constexpr int TILE = NT * 16;
   static constexpr int SLOTS = PA::ELEMS > PB::ELEMS ? PA::ELEMS : PB::ELEMS;

@@ -52,7 +52,13 @@ struct K5 {
   static constexpr int S = S0 < 2 ? 2 : (S0 > 4 ? 4 : S0);
   static constexpr bool TWS = N * BPC <= 65536 && S * TILE_BYTES0 + N * BPC <= 210 * 1024;
   // group-mode exchanges: a signal's TPS threads sync among themselves only
-  using F = Fft<T, N, EMAX, INV, false, -1, TWS>;
+  // generated radix-16 twiddles (Fft TWG): measured 2-3% faster from N = 2048
+  // (FP32 and FP64), 2% slower at 512 / 1024
+#ifndef TFFT_K5_TWG
+#define TFFT_K5_TWG -1
+#endif
+  static constexpr bool TWG = TFFT_K5_TWG < 0 ? LOGN >= 11 : TFFT_K5_TWG != 0;
+  using F = Fft<T, N, EMAX, INV, false, -1, TWS, TWG>;
   static constexpr int E = F::E;
   static constexpr int TPS = F::TPS;
   static constexpr int SPT = NT / TPS;  // signals per tile
@@ -202,10 +208,6 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
     if (tid < 32) tmem_alloc(tmem_base, K::TCOLS);
     tmem_fence_before();
   }
-  if constexpr (K::TWS) F::build_pass_tables(tws, static_cast<const CT*>(a.tw), tid, K::NTHR);
-  __syncthreads();
-  if constexpr (ABFT) tmem_fence_after();
-  const CT* tw = K::TWS ? tws : static_cast<const CT*>(a.tw);
 
   // tile sequence (identical in producer and consumers): plain = round robin;
   // ABFT = the segments of [lo, hi) in order, each in tiles of SPT signals
@@ -245,24 +247,35 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
     for (int gg = 0; gg < nsig; ++gg) bulk_g2s(dst + gg * K::SLOT, x + (s0 + gg) * N, N * K::BPC, &full[slot]);
   };
   Cursor pc = first();  // producer cursor (producer warp, or thread 0 when inline)
-  if constexpr (K::INL) {
-    if (tid == 0) {
-      int64_t s0;
-      int nsig;
-      for (int i = 0; i < S && next(pc, s0, nsig); ++i) land(i, s0, nsig);
-    }
-  } else if (tid >= NT) {
-    // ------------------------------------------------------------ producer
-    if (tid != NT) return;
+  // thread 0 lands the first S tiles before the CTA builds its twiddle
+  // tables, so the first loads' DRAM latency overlaps the table reads (small
+  // batches: C1 is ~7 tiles per CTA); the producer warp takes over from tile S
+  if (tid == 0) {
     int64_t s0;
     int nsig;
+    for (int i = 0; i < S && next(pc, s0, nsig); ++i) land(i, s0, nsig);
+  }
+  if constexpr (K::TWS) F::build_pass_tables(tws, static_cast<const CT*>(a.tw), tid, K::NTHR);
+  __syncthreads();
+  if constexpr (ABFT) tmem_fence_after();
+  const CT* tw = K::TWS ? tws : static_cast<const CT*>(a.tw);
+  if constexpr (!K::INL) {
+    if (tid >= NT) {
+      // ---------------------------------------------------------- producer
+      if (tid != NT) return;
+      int64_t s0;
+      int nsig;
+      int it = 0;
+      for (; it < S && next(pc, s0, nsig); ++it) {
+      }
 #pragma unroll 1
-    for (int it = 0; next(pc, s0, nsig); ++it) {
-      const int s = it % S;
-      if (it >= S) mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
-      land(s, s0, nsig);
+      for (; next(pc, s0, nsig); ++it) {
+        const int s = it % S;
+        mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
+        land(s, s0, nsig);
+      }
+      return;
     }
-    return;
   }
 
   // -------------------------------------------------------------- consumers
