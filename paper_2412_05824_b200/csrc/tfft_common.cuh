@@ -318,6 +318,19 @@ __device__ __forceinline__ void st_cs(double2* p, double2 v) { __stcs(p, v); }
 
 template <typename T> __device__ __forceinline__ bool finite2(C<T> v) { return isfinite(v.x) && isfinite(v.y); }
 
+// Non-finite detection on the integer pipe (isfinite of a double is two DSETP
+// on the half-rate FP64 pipe per element): nf_acc keeps the largest exponent
+// field seen, which is all-ones exactly when some value was Inf or NaN
+template <typename T> __device__ __forceinline__ unsigned nf_acc(unsigned acc, C<T> v) {
+  if constexpr (sizeof(T) == 8)
+    return __vimax3_u32(acc, (unsigned)__double2hiint(v.x) & 0x7ff00000u, (unsigned)__double2hiint(v.y) & 0x7ff00000u);
+  else
+    return __vimax3_u32(acc, __float_as_uint(v.x) & 0x7f800000u, __float_as_uint(v.y) & 0x7f800000u);
+}
+template <typename T> __device__ __forceinline__ bool nf_bad(unsigned acc) {
+  return acc == (sizeof(T) == 8 ? 0x7ff00000u : 0x7f800000u);
+}
+
 // XOR swizzle (element units) so Stockham scatter writes hit distinct banks:
 // 16 float2 / 8 double2 slots per 128-byte bank row.
 template <typename T> __device__ __forceinline__ int swz(int a) {

@@ -12,6 +12,11 @@
 
 #include "tfft_common.cuh"
 
+// TWG tables hold only the rows load_tw reads (1 = compact; 0 = every power)
+#ifndef TFFT_TW_COMPACT
+#define TFFT_TW_COMPACT 1
+#endif
+
 namespace tfft {
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
@@ -79,14 +84,25 @@ struct Fft {
   static constexpr int NPAD = N + (N >> LOGP);  // elements a slot buffer occupies
   static __device__ __forceinline__ int phys(int a) { return a + (a >> LOGP); }
 
+  // rows of pass P's block: every power t = 1..R-1, or with TWG only the
+  // powers load_tw reads (t = 1, 4, 8, 12 for radix 16; 1, 4 for 8; 1 below)
+  static constexpr bool CMP = TWG && TWS && TFFT_TW_COMPACT;
+  template <int R>
+  __host__ __device__ static constexpr int nrows() {
+    return !CMP ? R - 1 : (R >= 16 ? 4 : (R >= 8 ? 2 : 1));
+  }
+  // table row ri holds the power t = row_pow(ri)
+  __host__ __device__ static constexpr int row_pow(int ri) { return CMP ? (ri == 0 ? 1 : 4 * ri) : ri + 1; }
+
   // offset of pass P's block in the per-pass table: sum over earlier passes
-  // P' >= 1 of (R' - 1) S' (= S_P - E for P >= 1); PASS_TABLE entries in all
+  // P' >= 1 of rows(R') S' (= S_P - E for P >= 1 without TWG); PASS_TABLE
+  // entries in all
   template <int P>
   __host__ __device__ static constexpr int pass_off() {
     if constexpr (P <= 1) return 0;
-    else return pass_off<P - 1>() + (radix<P - 1>() - 1) * stride<P - 1>();
+    else return pass_off<P - 1>() + nrows<radix<P - 1>()>() * stride<P - 1>();
   }
-  static constexpr int PASS_TABLE = NPASS > 1 ? N - E : 0;
+  static constexpr int PASS_TABLE = NPASS > 1 ? pass_off<NPASS>() : 0;
 
   // per-pass twiddle tables from the global w_N table (direction included),
   // cooperatively by threads [tid0, tid0 + nthr)
@@ -100,8 +116,8 @@ struct Fft {
       constexpr int R = radix<P>();
       constexpr int S = stride<P>();
       constexpr int M = N / (S * R);
-      for (int i = tid; i < (R - 1) * S; i += nthr) {
-        const int t = i / S + 1, q = i % S;
+      for (int i = tid; i < nrows<R>() * S; i += nthr) {
+        const int t = row_pow(i / S), q = i % S;
         dst[pass_off<P>() + i] = wn[q * t * M];
       }
       build_from<P + 1>(dst, wn, tid, nthr);
@@ -118,18 +134,20 @@ struct Fft {
       for (int u = 0; u < E / R; ++u) {
         const int q = (tau + TPS * u) & (S - 1);
         if constexpr (TWG && TWS && R >= 4) {
-          const C<T>* b = tw + pass_off<P>() + q;  // w^t at b[(t - 1) * S]
+          // w^1, w^4, w^8, w^12 at b[0], b[S], b[2S], b[3S] (compact) or b[(t - 1) S]
+          const C<T>* b = tw + pass_off<P>() + q;
+          constexpr int S4 = CMP ? S : 3 * S, S8 = CMP ? 2 * S : 7 * S, S12 = CMP ? 3 * S : 11 * S;
           w[u * R + 1] = b[0];
           w[u * R + 2] = cmul<T>(w[u * R + 1], w[u * R + 1]);
           w[u * R + 3] = cmul<T>(w[u * R + 2], w[u * R + 1]);
           if constexpr (R >= 8) {
-            w[u * R + 4] = b[3 * S];
+            w[u * R + 4] = b[S4];
 #pragma unroll
             for (int t = 1; t < 4; ++t) w[u * R + 4 + t] = cmul<T>(w[u * R + 4], w[u * R + t]);
           }
           if constexpr (R == 16) {
-            w[u * R + 8] = b[7 * S];
-            w[u * R + 12] = b[11 * S];
+            w[u * R + 8] = b[S8];
+            w[u * R + 12] = b[S12];
 #pragma unroll
             for (int t = 1; t < 4; ++t) {
               w[u * R + 8 + t] = cmul<T>(w[u * R + 8], w[u * R + t]);

@@ -118,8 +118,18 @@ struct K4Item {
   int64_t r;
 };
 
-__device__ __forceinline__ K4Item k4_decode_ab(const K4Args& a, int64_t t) {
-  const int64_t ta = a.ta, tb = a.tb + a.tc, ng = a.ngroups, taL = a.ta_last, tbL = a.tb_last + a.tc_last;
+// ring slot of group g (3 slots). Tile and group indices stay below 2^32 (a
+// launch covers at most 2^31 elements of x), so the schedule arithmetic is
+// 32-bit: it runs per tile in every consumer thread
+__device__ __forceinline__ int64_t k4_slot(int64_t g) { return (unsigned)g % 3u; }
+
+// ticket t -> tile, in the order A(0) A(1) B(0) A(2) B(1) ... A(ng-1) B(ng-2)
+// B(ng-1). A ticket never waits for a later one (B(g) on A(g), A(g) on
+// B(g - 3)), so the schedule cannot deadlock whatever the grid.
+__device__ __forceinline__ K4Item k4_decode_ab(const K4Args& a, int64_t t64) {
+  const unsigned ta = (unsigned)a.ta, tb = (unsigned)(a.tb + a.tc), ng = (unsigned)a.ngroups;
+  const unsigned taL = (unsigned)a.ta_last, tbL = (unsigned)(a.tb_last + a.tc_last);
+  unsigned t = (unsigned)t64;
   if (ng == 1) {
     if (t < taL) return {0, 0, t};
     t -= taL;
@@ -127,14 +137,14 @@ __device__ __forceinline__ K4Item k4_decode_ab(const K4Args& a, int64_t t) {
     return {-1, 0, 0};
   }
   if (t < ta) return {0, 0, t};
-  const int64_t u = t - ta;
-  const int64_t h = u / (ta + tb) + 1;
+  const unsigned u = t - ta;
+  const unsigned h = u / (ta + tb) + 1;
   if (h <= ng - 2) {
-    const int64_t r = u - (h - 1) * (ta + tb);
+    const unsigned r = u - (h - 1) * (ta + tb);
     if (r < ta) return {0, h, r};
     return {1, h - 1, r - ta};
   }
-  int64_t r = t - (ta + (ng - 2) * (ta + tb));
+  unsigned r = t - (ta + (ng - 2) * (ta + tb));
   if (r < taL) return {0, ng - 1, r};
   r -= taL;
   if (r < tb) return {1, ng - 2, r};
@@ -157,7 +167,7 @@ __device__ __forceinline__ K4Item k4_decode(const K4Args& a, int64_t t) {
 }
 
 __device__ __forceinline__ bool k4_ready(const K4Args& a, const K4Item& it) {
-  if (it.phase == 0) {
+  if (it.phase == 0) {  // the group's ring slot: its previous occupant's B tiles are done
     if (it.g < 3) return true;
     return ld_acquire(a.done_b + (it.g - 3)) >= (unsigned)a.tb;
   }
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       } else {
         // the ring is column-blocked: pass-B tile (signal sl, block j) is one
         // contiguous run of N2 * CB_B elements
-        const CT* src = static_cast<const CT*>(a.z) + ((item.g % 3) * G + (r / ncbB)) * N +
+        const CT* src = static_cast<const CT*>(a.z) + (k4_slot(item.g) * G + (r / ncbB)) * N +
                         (int64_t)(r % ncbB) * K::TILE;
         mbar_expect_tx(&full[s], K::TILE * K::BPC);
         bulk_g2s(dst, src, K::TILE * K::BPC, &full[s]);
@@ -470,7 +480,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       P::F::run(slots + P::base(gA), v, tA, tws1);
 #endif
       // blocked ring layout: Z'[p][q] at ((q / CB_B) * N2 + p) * CB_B + q % CB_B
-      CT* d = z + ((cur.g % 3) * G + sl) * N + p * PB::CB;
+      CT* d = z + (k4_slot(cur.g) * G + sl) * N + p * PB::CB;
       TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));  // w_N^{p (tA + TPS j)}, j ascending
       const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
 #pragma unroll
@@ -498,7 +508,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       {
         // the tile's ring lines are dead now: drop them from L2 without a
         // write-back (the slot is fully rewritten by pass A three groups on)
-        const char* src = reinterpret_cast<const char*>(z + ((cur.g % 3) * G + (r / ncbB)) * N +
+        const char* src = reinterpret_cast<const char*>(z + (k4_slot(cur.g) * G + (r / ncbB)) * N +
                                                         (int64_t)(r % ncbB) * K::TILE);
 #pragma unroll 1
         for (int i = tid; i < K::TILE * K::BPC / 128; i += NT)
@@ -676,6 +686,16 @@ __device__ __forceinline__ void k7_tma_store(const CUtensorMap* map, const void*
                : "memory");
 }
 
+// the producer decodes each ticket once and hands the tile to the consumers
+// (and on to the releaser) packed in one word: phase << 62 | g << 32 | r
+// (g < 2^30 groups, r < 2^32 tiles); negative = no more tiles
+__device__ __forceinline__ long long k7_pack(const K4Item& it) {
+  return ((long long)it.phase << 62) | ((long long)it.g << 32) | (long long)(unsigned)it.r;
+}
+__device__ __forceinline__ K4Item k7_unpack(long long w) {
+  return {(int)(w >> 62), (int64_t)((w >> 32) & 0x3fffffff), (int64_t)(unsigned)w};
+}
+
 template <typename T, int L1, int L2, bool INV>
 __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
     k7_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmz,
@@ -736,7 +756,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
       mbar_wait_sleep(&done[i], (it / K::RR) & 1);
       const long long t = rtk[i];
       if (t < 0) return;
-      const K4Item c = k4_decode(a, t);
+      const K4Item c = k7_unpack(t);
       if constexpr (LDISC) {
         if (c.phase == 1 && a.line_cnt != nullptr) {
           constexpr int TPL = PB::LINE / PB::CB;  // tiles per line group
@@ -745,7 +765,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
           unsigned last = 0;
           if (lane == 0) last = atomicAdd(a.line_cnt + (c.g * G + sl) * (N1 / PB::LINE) + lg, 1u) == TPL - 1;
           if (__shfl_sync(0xffffffffu, last, 0)) {
-            const CT* base = static_cast<const CT*>(a.z) + ((c.g % 3) * G + sl) * N + lg * PB::LINE;
+            const CT* base = static_cast<const CT*>(a.z) + (k4_slot(c.g) * G + sl) * N + lg * PB::LINE;
 #pragma unroll 4
             for (int p = lane; p < N2; p += 32)
               asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (int64_t)p * N1) : "memory");
@@ -777,7 +797,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
         mbar_arrive(&full[0]);
         return;
       }
-      tk[0] = t;
+      tk[0] = k7_pack(item);
       const int r = (int)item.r;
       mbar_expect_tx(&full[0], K::TILE * K::ES);
       if (item.phase == 0) {
@@ -795,7 +815,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
         using P = PB;
         const int sl = r / ncbB;
         const int q0 = (r - sl * ncbB) * P::CB;
-        const int row0 = (int)(((item.g % 3) * G + sl) * N2);
+        const int row0 = (int)((k4_slot(item.g) * G + sl) * N2);
 #pragma unroll 1
         for (int cb = 0; cb < P::CB / P::BW; ++cb)
 #pragma unroll 1
@@ -814,7 +834,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
 
   // -------------------------------------------------------------- consumers
   CT* __restrict__ z = static_cast<CT*>(a.z);
-  bool bad = false;
+  unsigned nfx = 0;  // non-finite inputs (nf_acc)
   bool staged = false;  // the slots hold outputs a TMA store may still be reading
 #pragma unroll 1
   for (int it = 0;; ++it) {
@@ -828,7 +848,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
       if ((tid & 31) == 0) mbar_arrive(&done[ri]);
       break;
     }
-    const K4Item cur = k4_decode(a, t);
+    const K4Item cur = k7_unpack(t);
     CT v[16];
     const int r = (int)cur.r;
     if (cur.phase == 0) {
@@ -842,7 +862,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
       const int64_t sig = cur.g * G + sl;
       const int p = (r - sl * ncbA) * P::CB + g;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) bad |= !finite2<T>(v[k]);
+      for (int k = 0; k < 16; ++k) nfx = nf_acc<T>(nfx, v[k]);
       if (a.nfaults > 0) {
         for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
           const DevFault fl = a.faults[f];
@@ -869,7 +889,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
 #if !(TFFT_K7_EXP & 1)  // experiment: FFT arithmetic compiled out (data path only)
       P::F::run(slots + g * P::SLOTQ, v, tau, tws1, 2 + g);
 #endif
-      CT* d = z + ((cur.g % 3) * G + sl) * N + (int64_t)p * N1;  // p-major ring
+      CT* d = z + (k4_slot(cur.g) * G + sl) * N + (int64_t)p * N1;  // p-major ring
       TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));
       const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
 #pragma unroll
@@ -902,7 +922,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
           constexpr int LPR = P::CB / P::LINE;  // lines per ring row of the tile
           const int sl = r / ncbB;
           const int q0 = (r - sl * ncbB) * P::CB;
-          const CT* base = z + ((cur.g % 3) * G + sl) * N + q0;
+          const CT* base = z + (k4_slot(cur.g) * G + sl) * N + q0;
 #pragma unroll 1
           for (int i = tid; i < N2 * LPR; i += NT)
             asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (int64_t)(i / LPR) * N1 +
@@ -948,7 +968,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
     if ((tid & 31) == 0) mbar_arrive(&done[ri]);
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
+  if (__any_sync(0xffffffffu, nf_bad<T>(nfx)) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
 }
 
 template <typename T, int L1, int L2, bool INV>

@@ -282,7 +282,7 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
   const int g = tid / TPS;
   const int tau = tid % TPS;
   CT* __restrict__ y = static_cast<CT*>(a.y);
-  bool bad = false;
+  unsigned nfx = 0;  // non-finite inputs (nf_acc)
   // this thread's TMEM arrays: lane quadrant = warp % 4, column block = warpgroup
   const uint32_t tbase = ABFT ? (*tmem_base + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) +
                                  (uint32_t)((tid >> 7) * K::BLK))
@@ -309,7 +309,7 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
     for (int k = 0; k < E; ++k) v[k] = buf[tau + TPS * k];
     if (valid) {
 #pragma unroll
-      for (int k = 0; k < E; ++k) bad |= !finite2<T>(v[k]);
+      for (int k = 0; k < E; ++k) nfx = nf_acc<T>(nfx, v[k]);
     }
     double red5[5] = {0, 0, 0, 0, 0};
     if constexpr (ABFT) {
@@ -533,7 +533,7 @@ __device__ __forceinline__ void k5_body(const K1Args& a) {
     tmem_fence_after();
     if (tid < 32) tmem_dealloc(*tmem_base, K::TCOLS);
   }
-  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
+  if (__any_sync(0xffffffffu, nf_bad<T>(nfx)) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
 }
 
 template <typename T, int LOGN, bool INV, bool ABFT>
