@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
   const int gB = tid % PB::CB, tB = tid / PB::CB;
   CT* __restrict__ y = static_cast<CT*>(a.y);
   CT* __restrict__ z = static_cast<CT*>(a.z);
-  bool bad = false;
+  unsigned nfx = 0;  // non-finite inputs (nf_acc)
 
 #pragma unroll 1
   for (int it = 0;; ++it) {
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       const int64_t sig = cur.g * G + sl;
       const int p = (r - sl * ncbA) * P::CB + gA;
 #pragma unroll
-      for (int k = 0; k < E; ++k) bad |= !finite2<T>(v[k]);
+      for (int k = 0; k < E; ++k) nfx = nf_acc<T>(nfx, v[k]);
       if (a.nfaults > 0) {  // stage-0 strikes on the freshly loaded input (fault.py:99-107)
         for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
           const DevFault fl = a.faults[f];
@@ -482,21 +482,27 @@ __global__ void __launch_bounds__(NT + 64, MINB)
       // blocked ring layout: Z'[p][q] at ((q / CB_B) * N2 + p) * CB_B + q % CB_B
       CT* d = z + (k4_slot(cur.g) * G + sl) * N + p * PB::CB;
       TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));  // w_N^{p (tA + TPS j)}, j ascending
-      const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
+      constexpr int RL = P::F::RLAST;
+      // stage-1 strikes on the canonical intermediate, in one uniform branch
+      // outside the store loop (register k holds output position j)
+      if (a.nfaults > 0 && a.strike_stage == 1) {
+        for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
+          const DevFault fl = a.faults[f];
+          if (fl.stage != 1) continue;
 #pragma unroll
-      for (int j = 0; j < E; ++j) {
-        constexpr int RL = P::F::RLAST;
-        const int k = (j % (E / RL)) * RL + j / (E / RL);  // register holding output position j
-        const int q = tA + P::TPS * j;
-        if (a.nfaults > 0 && a.strike_stage == 1) {  // canonical stage-1 intermediate
-          for (int f = f1; f < a.nfaults && a.faults[f].signal == sig; ++f) {
-            const DevFault fl = a.faults[f];
-            if (fl.signal == sig && fl.stage == 1 && fl.element == q + (int64_t)p * N1) {
+          for (int j = 0; j < E; ++j) {
+            const int k = (j % (E / RL)) * RL + j / (E / RL);
+            if (fl.element == tA + P::TPS * j + (int64_t)p * N1) {
               if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
               else v[k].y = flip_bits(v[k].y, fl.bit);
             }
           }
         }
+      }
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const int k = (j % (E / RL)) * RL + j / (E / RL);
+        const int q = tA + P::TPS * j;
         d[(q / PB::CB) * (N2 * PB::CB) + (q % PB::CB)] = cmul<T>(v[k], w.next(j));
       }
     } else {
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&done[ri]);  // this warp's stores are issued
   }
-  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
+  if (__any_sync(0xffffffffu, nf_bad<T>(nfx)) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
 }
 
 template <typename T, int L1, int L2, bool INV, int E, int NT, int S, int MINB>
@@ -891,22 +897,27 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
 #endif
       CT* d = z + (k4_slot(cur.g) * G + sl) * N + (int64_t)p * N1;  // p-major ring
       TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));
-      const int f1 = (a.nfaults > 0 && a.strike_stage == 1) ? fault_lo(a.faults, a.nfaults, sig) : 0;
+      constexpr int RL = P::F::RLAST;
+      // stage-1 strikes on the canonical intermediate (before the four-step
+      // twiddle), in one uniform branch outside the store loop
+      if (a.nfaults > 0 && a.strike_stage == 1) {
+        for (int f = fault_lo(a.faults, a.nfaults, sig); f < a.nfaults && a.faults[f].signal == sig; ++f) {
+          const DevFault fl = a.faults[f];
+          if (fl.stage != 1) continue;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        constexpr int RL = P::F::RLAST;
-        const int k = (j % (16 / RL)) * RL + j / (16 / RL);
-        const int q = tau + P::TPS * j;
-        if (a.nfaults > 0 && a.strike_stage == 1) {
-          for (int f = f1; f < a.nfaults && a.faults[f].signal == sig; ++f) {
-            const DevFault fl = a.faults[f];
-            if (fl.signal == sig && fl.stage == 1 && fl.element == q + (int64_t)p * N1) {
+          for (int j = 0; j < 16; ++j) {
+            const int k = (j % (16 / RL)) * RL + j / (16 / RL);
+            if (fl.element == tau + P::TPS * j + (int64_t)p * N1) {
               if (fl.part == 0) v[k].x = flip_bits(v[k].x, fl.bit);
               else v[k].y = flip_bits(v[k].y, fl.bit);
             }
           }
         }
-        d[q] = cmul<T>(v[k], w.next(j));
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int k = (j % (16 / RL)) * RL + j / (16 / RL);
+        d[tau + P::TPS * j] = cmul<T>(v[k], w.next(j));
       }
     } else {
       using P = PB;
