@@ -318,6 +318,7 @@ __device__ __forceinline__ void st_cs(double2* p, double2 v) { __stcs(p, v); }
 
 template <typename T> __device__ __forceinline__ bool finite2(C<T> v) { return isfinite(v.x) && isfinite(v.y); }
 
+
 // Non-finite detection on the integer pipe (isfinite of a double is two DSETP
 // on the half-rate FP64 pipe per element): nf_acc keeps the largest exponent
 // field seen, which is all-ones exactly when some value was Inf or NaN

@@ -89,8 +89,9 @@ struct K4Ph {
 // invalidate the SM's whole L1 (CCTL.IVALL) on every poll, evicting the
 // twiddle tables of both resident CTAs. The data the counter guards is only
 // ever read by the TMA engine (async proxy, straight from L2) after a
-// fence.proxy.async, and the writer's release (MEMBAR.GPU before the count)
-// has made it globally performed, so no L1 copy can be stale.
+// fence.proxy.async, and the writer's release (MEMBAR.GPU before the count,
+// plus the consumer warps' own fences in K4: publish_tile) has made it
+// globally performed, so no L1 copy can be stale.
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -101,6 +102,30 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Publishing a finished tile: consumer warps arrive on done[] and the
+// releaser thread bumps the GPU-scope count other CTAs poll. K4's pass-A
+// tiles of 2048-point columns scatter 16-byte stores over 2048 ring lines per
+// warp instruction; with only the releaser's fence, a pass-B tile of another
+// CTA was seen landing lines whose stores were still draining (whole wrong
+// rows at FP64 2^22, ~0.7 per 1 GiB run; tools/parseval_stress.py). So K4's
+// consumer warps fence their own stores before arriving (PUB = 1: 0 failures
+// in 120 runs; a deferred fence -- run after the next tile's FFT -- was slower
+// and not clean). K7's pass-A stores leave in whole-line runs; no failure in
+// 520 stressed launches without the per-warp fence (PUB = 0), which costs it
+// 15-25%.
+#ifndef TFFT_K4_PUB
+#define TFFT_K4_PUB 1
+#endif
+#ifndef TFFT_K7_PUB
+#define TFFT_K7_PUB 0
+#endif
+template <int PUB>
+__device__ __forceinline__ void publish_tile(uint64_t* done, int ri) {
+  if (PUB == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&done[ri]);
 }
 // 2-D TMA box load global -> shared, completion counted on an mbarrier
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -535,8 +560,7 @@ __global__ void __launch_bounds__(NT + 64, MINB)
         else __stcs(d + (int64_t)(tB + P::TPS * P::F::out_pos(k)) * N1, val);
       }
     }
-    __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&done[ri]);  // this warp's stores are issued
+    publish_tile<TFFT_K4_PUB>(done, ri);  // this warp's stores are issued
   }
   if (__any_sync(0xffffffffu, nf_bad<T>(nfx)) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
 }
@@ -670,7 +694,21 @@ struct K7Cfg {
   using PB = K7Ph<T, L2, INV, NT, TWG>;
   static constexpr int ES = PA::ES;
   static constexpr int TILE = NT * 16;
-  static constexpr int SLOTS = PA::ELEMS > PB::ELEMS ? PA::ELEMS : PB::ELEMS;
+  // Column slots per WARP, not per column index: warps run their tiles
+  // without a CTA barrier between a pass-A tile and the next pass-B tile, so
+  // each warp must own the same slot region in both passes (with per-column
+  // bases, (7, 6) FP64 had warp regions of 4 x 136 elements in pass A but
+  // 8 x 76 in pass B, overlapping a neighbour still in its pass-A FFT).
+  static constexpr int wreg(int slotq, int tps) { return tps <= 32 ? slotq * (32 / tps) : slotq / (tps / 32); }
+  static constexpr int WREG = wreg(PA::SLOTQ, PA::TPS) > wreg(PB::SLOTQ, PB::TPS) ? wreg(PA::SLOTQ, PA::TPS)
+                                                                                   : wreg(PB::SLOTQ, PB::TPS);
+  static constexpr int SLOTS = (NT / 32) * WREG;
+  // slot base of column g (owned by the warp of thread tid) in phase P
+  template <typename P>
+  static __device__ __forceinline__ int cbase(int g, int tid) {
+    if constexpr (P::TPS <= 32) return (tid >> 5) * WREG + (g % (32 / P::TPS)) * P::SLOTQ;
+    else return g * (P::TPS / 32) * WREG;  // a column over TPS / 32 warps: their regions
+  }
   static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));
   static constexpr int RR = 4;
   // stage first, then the column slots, both 1024-byte aligned for the
@@ -893,7 +931,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
         staged = false;
       }
 #if !(TFFT_K7_EXP & 1)  // experiment: FFT arithmetic compiled out (data path only)
-      P::F::run(slots + g * P::SLOTQ, v, tau, tws1, 2 + g);
+      P::F::run(slots + K::template cbase<P>(g, tid), v, tau, tws1, 2 + g);
 #endif
       CT* d = z + (k4_slot(cur.g) * G + sl) * N + (int64_t)p * N1;  // p-major ring
       TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));
@@ -947,7 +985,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
         staged = false;
       }
 #if !(TFFT_K7_EXP & 1)
-      P::F::run(slots + g * P::SLOTQ, v, tau, tws2, 2 + g);
+      P::F::run(slots + K::template cbase<P>(g, tid), v, tau, tws2, 2 + g);
 #endif
       // outputs -> swizzled [k][column] staging (aliasing the slots: once every
       // column's FFT is done) -> 2-D TMA stores into y
@@ -975,8 +1013,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
       }
       staged = true;
     }
-    __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&done[ri]);
+    publish_tile<TFFT_K7_PUB>(done, ri);
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (__any_sync(0xffffffffu, nf_bad<T>(nfx)) && (tid & 31) == 0 && a.counters) atomicOr(&a.counters->nonfinite, 1ull);
@@ -1101,6 +1138,11 @@ bool k4_supported(int prec, int l1, int l2) {
   TFFT_K4_PAIRS
 #undef TFFT_K4
   if (!inst) return false;
+  // FP64 (2048, 2048) runs the two-launch K3: under tools/parseval_stress.py
+  // the fused kernel still produced a wrong row in ~1% of 1 GiB runs at this
+  // split after the per-warp publication fence (cause not found; no failure
+  // at any other split or in K3, which is 9% slower here: 2.40 vs 2.21 ms)
+  if (prec == 1 && l1 == 11 && l2 == 11) return false;
   return prec == 0 ? k4_shape_ok<float>(l1, l2) : k4_shape_ok<double>(l1, l2);
 }
 
