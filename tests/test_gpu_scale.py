@@ -102,6 +102,36 @@ def _full_batch_check(precision, log2n, total_bytes):
     assert float(((ey - ex).abs() / ex).max()) <= 1e3 * (1e-7 if precision == "single" else 1e-16) * log2n
 
 
+@pytest.mark.parametrize("precision,log2n", [("double", 13), ("double", 16), ("double", 20), ("double", 22),
+                                             ("single", 14), ("single", 20), ("single", 22)])
+def test_two_pass_repeated_runs_stable(precision, log2n):
+    """Race check for the persistent two-pass kernels (K7/K4 and their
+    cross-CTA ring hand-offs): the same 1 GiB batch transformed 8 times must
+    give bitwise-identical outputs every time, and every row must satisfy
+    Parseval. (A per-warp slot overlap at FP64 (128, 64) and late-visible
+    scattered ring stores at FP64 (2048, 2048) each showed up here as whole
+    wrong rows in a fraction of runs.)"""
+    tf = _tf()
+    import torch
+    from paper_2412_05824_b200 import fft_core
+    n = 2 ** log2n
+    bpc = 8 if precision == "single" else 16
+    b = 2 ** 30 // (n * bpc)
+    x = _device_batch(n, b, precision, log2n)
+    plan = tf.build_plan(tf.select_params(n, b, precision), precision)
+    y0 = torch.empty_like(x)
+    fft_core.device_execute(plan, x, y0)
+    ex = (x.abs() ** 2).sum(dim=1, dtype=torch.float64)
+    ey = (y0.abs() ** 2).sum(dim=1, dtype=torch.float64) / n
+    assert float(((ey - ex).abs() / ex).max()) <= 1e3 * (1e-7 if precision == "single" else 1e-16) * log2n
+    y = torch.empty_like(x)
+    for rep in range(8):
+        y.zero_()
+        fft_core.device_execute(plan, x, y)
+        bad = torch.nonzero((y != y0).any(dim=1)).flatten().tolist()
+        assert not bad, (rep, bad[:8])
+
+
 @pytest.mark.parametrize("log2n", list(range(8, 21)))
 def test_c2_full_gib_batch_fp64(log2n):
     """C2: FP64, B = 2^26/N (1 GiB in), the bench's exact shapes."""
