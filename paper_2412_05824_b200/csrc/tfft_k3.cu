@@ -896,7 +896,17 @@ static int64_t k4_group(const K3Plan* p, int64_t batch) {
   // ~16 MB of intermediate per group (3-slot ring ~48 MB) up to 2^16; 32 MB
   // from 2^17 (measured sweep 4..48 MB: 2^18..2^20 FP64 2-4% and FP32 3-7%
   // faster, 2^14..2^16 slower with the larger ring)
-  const int64_t mb = p->n >= (int64_t(1) << 17) ? 32 : 16;
+  // per-size group bytes from a sweep of the current K7 (tools/k7_sched_sweep.sh,
+  // 12..40 MB): 1-2% at FP64 2^17, 2^18 (20 MB), FP64 2^20 (16 MB: one signal
+  // per group, 0.770 vs 0.787 ms) and FP32 2^20 (24 MB: three signals)
+  int64_t mb = p->n >= (int64_t(1) << 17) ? 32 : 16;
+  if (p->prec == 1 && (p->n == (int64_t(1) << 17) || p->n == (int64_t(1) << 18))) mb = 20;
+  if (p->prec == 1 && p->n == (int64_t(1) << 20)) mb = 16;
+  if (p->prec == 0 && p->n == (int64_t(1) << 20)) mb = 24;
+  if (const char* env = std::getenv("TFFT_K4_GROUP_MB")) {  // tuning hook (tools/k7_sched_sweep.sh)
+    const long long v = std::atoll(env);
+    if (v >= 1 && v <= 256) mb = v;
+  }
   int64_t g = (mb << 20) / (p->n * cb);
   if (g < 1) g = 1;
   if (g > batch) g = batch;

@@ -44,6 +44,21 @@ def rel_l2(got, ref):
     return float(np.linalg.norm((got - ref).ravel()) / max(np.linalg.norm(ref.ravel()), 1e-300))
 
 
+def two_pass_group(precision, n):
+    """Signals per ring group of the fused two-pass kernels (mirrors
+    tfft_k3.cu k4_group): 16 MB of intermediate below 2^17, 32 MB from 2^17,
+    with the per-size exceptions of the measured sweep."""
+    bpc = 8 if precision == "single" else 16
+    mb = 32 if n >= 2 ** 17 else 16
+    if precision == "double" and n in (2 ** 17, 2 ** 18):
+        mb = 20
+    if precision == "double" and n == 2 ** 20:
+        mb = 16
+    if precision == "single" and n == 2 ** 20:
+        mb = 24
+    return max(1, (mb << 20) // (n * bpc))
+
+
 def l2_tol(precision, n):
     """BASELINE.json north_star: 1e-5 log2N (FP32) / 1e-12 log2N (FP64)."""
     return (1e-5 if precision == "single" else 1e-12) * max(np.log2(n), 1.0)

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from conftest import (EPS, gaussian, golden, golden_abft_outputs, golden_fft_outputs, l2_tol, max_rel_error,
-                      oracle_tol, rel_l2)
+                      oracle_tol, rel_l2, two_pass_group)
 
 pytestmark = pytest.mark.gpu
 
@@ -233,7 +233,7 @@ def test_fused_two_pass_many_groups(precision, log2n, groups):
     tf = _tf()
     n = 2 ** log2n
     bpc = 8 if precision == "single" else 16
-    g = max(1, ((32 if n >= 2 ** 17 else 16) << 20) // (n * bpc))  # K4 group size (tfft_k3.cu k4_group)
+    g = two_pass_group(precision, n)  # ring group size (tfft_k3.cu k4_group)
     b = g * groups + max(1, g // 3)
     x = gaussian(n, b, precision, seed=log2n + 100)
     plan = tf.build_plan(tf.select_params(n, b, precision), precision)

@@ -20,7 +20,7 @@ from functools import lru_cache
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, gaussian, l2_tol, max_rel_error, oracle_tol, rel_l2
+from conftest import GOLDEN, gaussian, l2_tol, max_rel_error, oracle_tol, rel_l2, two_pass_group
 
 pytestmark = pytest.mark.gpu
 
@@ -85,7 +85,7 @@ def _full_batch_check(precision, log2n, total_bytes):
     plan = tf.build_plan(tf.select_params(n, b, precision), precision)
     y = tf.execute_plan(plan, tf.SignalBatch(x)).data
     torch.cuda.synchronize()
-    g = max(1, ((32 if n >= 2 ** 17 else 16) << 20) // (n * bpc))  # two-pass group size (tfft_k3.cu k4_group)
+    g = two_pass_group(precision, n)  # ring group size (tfft_k3.cu k4_group)
     rows = _sample_rows(b, g if b > g else None, k=64 if n <= 2 ** 16 else 16, seed=log2n)
     idx = torch.tensor(rows, device="cuda")
     xs = x.index_select(0, idx).cpu().numpy()
