@@ -121,6 +121,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef TFFT_K7_PUB
 #define TFFT_K7_PUB 0
 #endif
+#ifndef TFFT_K7_TILED
+#define TFFT_K7_TILED 1
+#endif
 template <int PUB>
 __device__ __forceinline__ void publish_tile(uint64_t* done, int ri) {
   if (PUB == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -711,6 +714,18 @@ struct K7Cfg {
   }
   static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));
   static constexpr int RR = 4;
+  // Tile-major ring for pass-B tiles narrower than a 128-byte line (CB_B <
+  // LINE: FP64 N2 >= 512, FP32 N2 >= 1024): Z''[(q / CB_B) N2 CB_B + p CB_B +
+  // q % CB_B], so each pass-B tile reads one contiguous N2 * CB_B block and
+  // discards it in whole lines after landing it. In the p-major layout such a
+  // tile owns only CB_B columns of each line it reads: the dirty lines cannot
+  // be dropped and are written back (2^20 FP64, 16 MB groups: 3.36 GB DRAM
+  // per launch for 2.15 GB algorithmic; 2.33 GB tile-major). But the kernel
+  // is latency-bound, not DRAM-bound, and the tile-major pass-A stores leave
+  // in CB_B-element runs (32-64 B instead of 256 B and more): measured faster
+  // only at FP64 (256, 512) (2^17: 0.606 vs 0.646 ms), 3-9% slower at every
+  // other narrow split, FP32 included -- so only that split uses it.
+  static constexpr bool TILED = TFFT_K7_TILED && PB::CB < PB::LINE && sizeof(T) == 8 && L1 == 8 && L2 == 9;
   // stage first, then the column slots, both 1024-byte aligned for the
   // 128-byte swizzle; pass-B outputs are staged in the slots (after the
   // column FFTs are done), so no separate staging buffer is needed
@@ -791,7 +806,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
     // last one drops the group's N2 lines from L2 without write-back (the
     // consumers discard whole-line tiles themselves), before publishing the
     // tile, so pass A of group g + 3 rewrites the slot only after the discard.
-    constexpr bool LDISC = PB::CB < PB::LINE;
+    constexpr bool LDISC = !K::TILED && PB::CB < PB::LINE;
     if (!LDISC && tid != NT + 32) return;
     const int lane = tid & 31;
 #pragma unroll 1
@@ -859,12 +874,15 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
         using P = PB;
         const int sl = r / ncbB;
         const int q0 = (r - sl * ncbB) * P::CB;
-        const int row0 = (int)((k4_slot(item.g) * G + sl) * N2);
+        // tile-major ring: the tile is rows [row0, row0 + N2) of CB_B columns
+        const int row0 = K::TILED ? (int)(((k4_slot(item.g) * G + sl) * ncbB + q0 / P::CB) * N2)
+                                  : (int)((k4_slot(item.g) * G + sl) * N2);
+        const int col0 = K::TILED ? 0 : q0;
 #pragma unroll 1
         for (int cb = 0; cb < P::CB / P::BW; ++cb)
 #pragma unroll 1
           for (int b = 0; b < P::NBOX; ++b)
-            tma_load_2d(stage + cb * (N2 * P::BW) + b * P::BOXR * P::BW, &tmz, (q0 + cb * P::BW) * 2,
+            tma_load_2d(stage + cb * (N2 * P::BW) + b * P::BOXR * P::BW, &tmz, (col0 + cb * P::BW) * 2,
                         row0 + b * P::BOXR, &full[0]);
       }
       t = t2;
@@ -933,7 +951,8 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
 #if !(TFFT_K7_EXP & 1)  // experiment: FFT arithmetic compiled out (data path only)
       P::F::run(slots + K::template cbase<P>(g, tid), v, tau, tws1, 2 + g);
 #endif
-      CT* d = z + (k4_slot(cur.g) * G + sl) * N + (int64_t)p * N1;  // p-major ring
+      constexpr int CBB = PB::CB;
+      CT* d = z + (k4_slot(cur.g) * G + sl) * N + (int64_t)p * (K::TILED ? CBB : N1);
       TwRun<T> w(cmul<T>(bh, bl), cmul<T>(sh, sl_));
       constexpr int RL = P::F::RLAST;
       // stage-1 strikes on the canonical intermediate (before the four-step
@@ -955,7 +974,8 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int k = (j % (16 / RL)) * RL + j / (16 / RL);
-        d[tau + P::TPS * j] = cmul<T>(v[k], w.next(j));
+        const int q = tau + P::TPS * j;
+        d[K::TILED ? (int64_t)(q / CBB) * (N2 * CBB) + q % CBB : (int64_t)q] = cmul<T>(v[k], w.next(j));
       }
     } else {
       using P = PB;
@@ -967,7 +987,13 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
       {
         // the tile's ring lines are dead: CB_B columns of N2 rows, 128-byte
         // lines hold LINE columns, so only whole-line tiles (CB_B >= LINE) discard
-        if constexpr (P::CB >= P::LINE) {
+        if constexpr (K::TILED) {
+          // tile-major ring: the tile is one contiguous block of N2 * CB_B elements
+          const CT* base = z + ((int64_t)k4_slot(cur.g) * G * ncbB + r) * (N2 * P::CB);
+#pragma unroll 1
+          for (int i = tid; i < N2 * P::CB / P::LINE; i += NT)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (int64_t)i * P::LINE) : "memory");
+        } else if constexpr (P::CB >= P::LINE) {
           constexpr int LPR = P::CB / P::LINE;  // lines per ring row of the tile
           const int sl = r / ncbB;
           const int q0 = (r - sl * ncbB) * P::CB;
@@ -1045,9 +1071,14 @@ static int launch_k7_t(const K4Args& a, int num_sms, cudaStream_t st) {
   // x: (B N1) rows of N2; ring: (3 G N2) rows of N1 (p-major); y: (B N2) rows of N1
   int rc = k4_encode_2d(&tmx, dt, const_cast<void*>(a.x), (uint64_t)(2 << L2), (uint64_t)a.batch << L1,
                         es << L2, (uint32_t)(2 * K::PA::BW), (uint32_t)K::PA::BOXR, K::PA::SWZ);
-  if (!rc)
-    rc = k4_encode_2d(&tmz, dt, a.z, (uint64_t)(2 << L1), (uint64_t)(3 * a.group) << L2, es << L1,
-                      (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
+  if (!rc) {
+    if (K::TILED)  // tile-major ring: (3 G N / CB_B) rows of CB_B columns
+      rc = k4_encode_2d(&tmz, dt, a.z, (uint64_t)(2 * K::PB::CB), ((uint64_t)(3 * a.group) << (L1 + L2)) / K::PB::CB,
+                        es * K::PB::CB, (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
+    else
+      rc = k4_encode_2d(&tmz, dt, a.z, (uint64_t)(2 << L1), (uint64_t)(3 * a.group) << L2, es << L1,
+                        (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
+  }
   if (!rc)
     rc = k4_encode_2d(&tmy, dt, a.y, (uint64_t)(2 << L1), (uint64_t)a.batch << L2, es << L1,
                       (uint32_t)(2 * K::PB::BW), (uint32_t)K::PB::BOXR, K::PB::SWZ);
