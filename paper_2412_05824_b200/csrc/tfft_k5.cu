@@ -26,6 +26,12 @@
 #ifndef TFFT_K5_EXP
 #define TFFT_K5_EXP 0
 #endif
+// deepest landing ring (tiles in flight per CTA): FP32 2 (a shallower ring
+// lets more CTAs share an SM; FP32 2^9 0.382 -> 0.349 ms, 2^11 0.358 -> 0.346,
+// tools/ab_interleave.sh), FP64 4 (2 measured 0.3-0.6% slower)
+#ifndef TFFT_K5_SMAX
+#define TFFT_K5_SMAX (sizeof(T) == 4 ? 2 : 4)
+#endif
 #ifndef TFFT_K5_FP64_E4096
 #define TFFT_K5_FP64_E4096 16
 #endif
@@ -49,7 +55,7 @@ struct K5 {
   static constexpr int SPT0 = NT / TPS0;
   static constexpr int TILE_BYTES0 = SPT0 * SLOT0 * BPC;
   static constexpr int S0 = 100 * 1024 / TILE_BYTES0;
-  static constexpr int S = S0 < 2 ? 2 : (S0 > 4 ? 4 : S0);
+  static constexpr int S = S0 < 2 ? 2 : (S0 > TFFT_K5_SMAX ? TFFT_K5_SMAX : S0);
   static constexpr bool TWS = N * BPC <= 65536 && S * TILE_BYTES0 + N * BPC <= 210 * 1024;
   // group-mode exchanges: a signal's TPS threads sync among themselves only
   // generated radix-16 twiddles (Fft TWG): measured 2-3% faster from N = 2048
