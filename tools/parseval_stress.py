@@ -1,5 +1,5 @@
 """Repeat full 1 GiB transforms and count rows whose energy breaks Parseval
-(a cheap full-batch integrity check): env PS_LOGN, PS_PREC, PS_REPS."""
+(a cheap full-batch integrity check): env PS_LOGN, PS_PREC, PS_REPS, PS_INV."""
 import os
 import sys
 from pathlib import Path
@@ -14,6 +14,7 @@ def main():
     prec = os.environ.get("PS_PREC", "double")
     dt, rdt, bpc = ((torch.complex64, torch.float32, 8) if prec == "single" else (torch.complex128, torch.float64, 16))
     tol = 1e3 * (1e-7 if prec == "single" else 1e-16)
+    inv = bool(int(os.environ.get("PS_INV", "0")))  # inverse: y = x * ... / n, so Parseval scales by 1/n
     for logn in [int(v) for v in os.environ.get("PS_LOGN", "13,14,16,20").split(",")]:
         n = 1 << logn
         b = (1 << 30) // (n * bpc)
@@ -24,8 +25,8 @@ def main():
         bad = []
         for rep in range(int(os.environ.get("PS_REPS", "5"))):
             y.zero_()
-            fft_core.device_execute(plan, x, y)
-            ey = (y.abs() ** 2).sum(dim=1, dtype=torch.float64) / n
+            fft_core.device_execute(plan, x, y, inverse=inv)
+            ey = (y.abs() ** 2).sum(dim=1, dtype=torch.float64) * (n if inv else 1.0 / n)
             err = (ey - ex).abs() / ex
             nb = int((err > tol * logn).sum())
             rows = torch.nonzero(err > tol * logn).flatten()[:8].tolist()
