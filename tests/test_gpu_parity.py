@@ -207,6 +207,38 @@ def test_two_pass_sizes_vs_oracle(precision, log2n):
     assert max_rel_error(back, x) <= (1e-5 if precision == "single" else 1e-12)
 
 
+@pytest.mark.parametrize("precision,log2n", [("double", 14), ("double", 16), ("double", 17), ("double", 18),
+                                             ("double", 20), ("double", 21), ("single", 14), ("single", 17),
+                                             ("single", 20), ("single", 22)])
+def test_two_pass_stage_strikes_vs_oracle(precision, log2n):
+    """Stage-0 and stage-1 strikes executed inside the fused two-pass kernels
+    (K7, K4; K7's tile-major ring at FP64 2^17) land on the same canonical
+    intermediate as the reference's strike hook (fault.py:99-107): the struck
+    transform equals the oracle's struck transform."""
+    tf = _tf()
+    from oracle import ref_oracle as O
+    n = 2 ** log2n
+    b = 3
+    x = gaussian(n, b, precision, seed=log2n + 7)
+    params = tf.select_params(n, b, precision)
+    assert len(params.spans) == 2
+    plan = tf.build_plan(params, precision)
+    y_clean = tf.execute_plan(plan, tf.SignalBatch(x)).data
+    bit = 52 if precision == "double" else 23  # lowest exponent bit: a factor of 2 (or 1/2)
+    for stage, elem in ((0, n // 3 + 5), (1, n - 7), (1, 12345 % n)):
+        sig = 1
+        tx = sig // plan.bs
+        inj = tf.FaultInjector(seu=False)
+        inj.arm(tf.FaultSpec(transaction=tx, signal=sig, element=elem, stage=stage, part="re", bit=bit),
+                plan=plan, batch=tf.SignalBatch(x))
+        y = tf.execute_plan(plan, tf.SignalBatch(x), injector=inj).data
+        ref = O.execute(x, O.select_params(n, b, precision), faults=[O.Fault(tx, sig, elem, stage, "re", bit)])
+        assert rel_l2(y, ref) <= l2_tol(precision, n), (stage, elem)
+        assert not np.array_equal(y[sig], y_clean[sig]), "the strike landed"
+        others = [r for r in range(b) if r != sig]
+        assert np.array_equal(y[others], y_clean[others]), "only the struck signal changes"
+
+
 @pytest.mark.parametrize("precision", ["single", "double"])
 def test_multipass_beyond_two_pass(precision):
     """N = 2^23 (three-stage curated plan) via the reference-order device passes."""
