@@ -731,7 +731,20 @@ def cpu_reference(sizes, fraction, workers, steps=1, warmup=0):
               f"{fraction:g} of each 1 GiB batch (B=2^26/N*{fraction:g}), FP64, forward; "
               f"resilient_fft execute_plan driver restated in oracle/ref_oracle.py")
     return {"value": round(flops / t / 1e9, 3), "unit": "GFLOP/s", "cores": workers, "kind": kind,
-            "sample": sample, "seconds": round(t, 2)}
+            "sample": sample, "seconds": round(t, 2), "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    """The host CPU the baseline ran on (model name, logical CPUs visible)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model} ({os.cpu_count()} logical CPUs)"
 
 
 def run_reference(args, dist):
