@@ -110,11 +110,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // warp instruction; with only the releaser's fence, a pass-B tile of another
 // CTA was seen landing lines whose stores were still draining (whole wrong
 // rows at FP64 2^22, ~0.7 per 1 GiB run; tools/parseval_stress.py). So K4's
-// consumer warps fence their own stores before arriving (PUB = 1: 0 failures
-// in 120 runs; a deferred fence -- run after the next tile's FFT -- was slower
-// and not clean). K7's pass-A stores leave in whole-line runs; no failure in
-// 520 stressed launches without the per-warp fence (PUB = 0), which costs it
-// 15-25%.
+// consumer warps fence their own stores before arriving (PUB = 1; a deferred
+// fence -- run after the next tile's FFT -- was slower and not clean). The
+// fence cut that split's failures to ~1% of runs but not to zero, so FP64
+// (2048, 2048) runs K3 (k4_supported); the splits K4 still serves showed no
+// failure in 150 runs each even without the fence, which is kept as the
+// conservative choice. K7's pass-A stores leave in whole-line runs; no
+// failure in 520+ stressed launches without the per-warp fence (PUB = 0),
+// which would cost it 15-25%.
 #ifndef TFFT_K4_PUB
 #define TFFT_K4_PUB 1
 #endif
