@@ -978,7 +978,11 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
       for (int j = 0; j < 16; ++j) {
         const int k = (j % (16 / RL)) * RL + j / (16 / RL);
         const int q = tau + P::TPS * j;
+#if !(TFFT_K7_EXP & 4)  // experiment: no ring stores (timing only)
         d[K::TILED ? (int64_t)(q / CBB) * (N2 * CBB) + q % CBB : (int64_t)q] = cmul<T>(v[k], w.next(j));
+#else
+        if (v[k].x == (T)12345.678) d[q] = cmul<T>(v[k], w.next(j));
+#endif
       }
     } else {
       using P = PB;
@@ -1028,7 +1032,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
       }
       fence_proxy_async();
       fft_sync<NT>();
-      if (tid == 0) {
+      if (tid == 0 && !(TFFT_K7_EXP & 8)) {  // experiment bit 8: no output TMA stores (timing only)
         const int sl = r / ncbB;
         const int q0 = (r - sl * ncbB) * P::CB;
         const int row0 = (int)((cur.g * G + sl) * N2);
