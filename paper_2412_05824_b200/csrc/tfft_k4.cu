@@ -127,6 +127,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef TFFT_K7_TILED
 #define TFFT_K7_TILED 1
 #endif
+// 1: stage K7's pass-B outputs in the column slots at every split with
+// 1024-point columns (the old rule); 0: FP32 uses a staging buffer of its own
+// where it fits two CTAs per SM
+#ifndef TFFT_K7_ALIAS_ALWAYS
+#define TFFT_K7_ALIAS_ALWAYS 0
+#endif
 template <int PUB>
 __device__ __forceinline__ void publish_tile(uint64_t* done, int ri) {
   if (PUB == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -700,6 +706,7 @@ struct K7Cfg {
   using PB = K7Ph<T, L2, INV, NT, TWG>;
   static constexpr int ES = PA::ES;
   static constexpr int TILE = NT * 16;
+  static constexpr int AL0 = 1024 / (int)sizeof(C<T>);  // 1024-byte alignment of the swizzled regions
   // Column slots per WARP, not per column index: warps run their tiles
   // without a CTA barrier between a pass-A tile and the next pass-B tile, so
   // each warp must own the same slot region in both passes (with per-column
@@ -715,7 +722,8 @@ struct K7Cfg {
     if constexpr (P::TPS <= 32) return (tid >> 5) * WREG + (g % (32 / P::TPS)) * P::SLOTQ;
     else return g * (P::TPS / 32) * WREG;  // a column over TPS / 32 warps: their regions
   }
-  static constexpr int TWE = (1 << L1) + (L1 == L2 ? 0 : (1 << L2));
+  static constexpr int TW1 = PA::F::PASS_TABLE;  // pass-B tables follow pass A's
+  static constexpr int TWE = TW1 + (L1 == L2 ? 0 : PB::F::PASS_TABLE);
   static constexpr int RR = 4;
   // Tile-major ring for pass-B tiles narrower than a 128-byte line (CB_B <
   // LINE: FP64 N2 >= 512, FP32 N2 >= 1024): Z''[(q / CB_B) N2 CB_B + p CB_B +
@@ -734,7 +742,12 @@ struct K7Cfg {
   // column FFTs are done), so no separate staging buffer is needed
   // (1024-point columns only: at <= 512 points a separate staging buffer still
   // fits two CTAs per SM and saves the wait for the stores' smem reads)
-  static constexpr bool ALIAS = L1 >= 10 || L2 >= 10;
+  static constexpr int SMEM_SEP = (2 * TILE + ((SLOTS + AL0 - 1) / AL0) * AL0 + TWE) * ES + 16 + RR * 24 + 1024 + 256;
+  // FP32: a buffer of its own where it fits two CTAs per SM (compact twiddle
+  // tables make room): 2^19 0.739 -> 0.725 ms, 2^20 0.779 -> 0.773; FP64
+  // measured 0.5-1.4% slower that way and keeps the aliased staging
+  static constexpr bool ALIAS =
+      (L1 >= 10 || L2 >= 10) && (TFFT_K7_ALIAS_ALWAYS || sizeof(T) == 8 || SMEM_SEP > 113 * 1024);
   static constexpr int SLOTS_AL = (SLOTS > TILE ? SLOTS : TILE);
   static constexpr int AL = 1024 / ES;  // 1024-byte alignment of the swizzled regions
   static constexpr int SLOTS_SZ = (SLOTS_AL + AL - 1) / AL * AL;
@@ -779,7 +792,7 @@ __global__ void __launch_bounds__(K7Nt<T>::NT + 64, 2)
   CT* slots = stage + K::TILE;
   CT* ystage = K::ALIAS ? slots : slots + K::SLOTS_SZ;  // pass-B output staging
   CT* tws1 = slots + K::SLOTS_SZ + (K::ALIAS ? 0 : K::TILE);
-  CT* tws2 = L1 == L2 ? tws1 : tws1 + N1;
+  CT* tws2 = L1 == L2 ? tws1 : tws1 + K::TW1;
   uint64_t* full = reinterpret_cast<uint64_t*>(tws1 + K::TWE);
   uint64_t* empty = full + 1;
   uint64_t* done = empty + 1;
